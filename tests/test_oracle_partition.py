@@ -1,0 +1,197 @@
+"""Pins for oracle/partition.py (§6; Table 3)."""
+from fractions import Fraction
+import itertools
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle.graph import normalized_adjacency
+from oracle.partition import (PartitionCfg, build_plan, ebv_partition, edge_order, eva_exact,
+                              outer_reduction, partition, stats)
+from synth import small_random_graph
+from tests.conftest import golden
+
+
+def test_spec_eva_examples(spec_examples):
+    ex = spec_examples["eva"]
+    V, E, p = ex["V"], ex["E"], ex["p"]
+    host = ex["host_of"]
+    g = Fraction(*ex["gamma"])
+    d_rep = [set() for _ in range(V)]
+    h_rep = [set() for _ in range(V)]
+    e_count = [0] * p
+    v_count = [0] * p
+    for i in range(p):
+        assert eva_exact(0, 1, i, d_rep, h_rep, host, e_count, v_count, E, V, p,
+                         gamma=g) == ex["empty_state_score"]
+    # assign (0,1) -> part 0
+    e_count[0] = 1
+    v_count[0] = 2
+    for x in (0, 1):
+        d_rep[x].add(0)
+        h_rep[x].add(host[0])
+    r = ex["after_edge_0_1_to_part_0"]
+    assert eva_exact(0, 2, 0, d_rep, h_rep, host, e_count, v_count, E, V, p, gamma=g) \
+        == Fraction(r["eva_0_2_part0"]).limit_denominator(1000)
+    assert eva_exact(0, 2, 1, d_rep, h_rep, host, e_count, v_count, E, V, p, gamma=g) \
+        == Fraction(r["eva_0_2_part1"]).limit_denominator(1000)
+    # single-host collapse (reading R22): host term i-independent -> 0.9*2 + 0.1*(0+1) = 1.9
+    assert eva_exact(0, 2, 1, d_rep, h_rep, [0, 0], e_count, v_count, E, V, p, gamma=g) \
+        == Fraction(19, 10)
+
+
+def _brute_greedy(n, eu, ev, cfg):
+    """Independent re-run of the greedy rule using the real-valued Eva
+    (fractions) and Python sets instead of the oracle's integer scores and bitmasks."""
+    host = cfg.hosts()
+    p = cfg.p
+    d_rep = [set() for _ in range(n)]
+    h_rep = [set() for _ in range(n)]
+    e_count = [0] * p
+    v_count = [0] * p
+    first = [None] * n
+    out = [None] * len(eu)
+    for e in edge_order(n, eu, ev, cfg):
+        u, v = int(eu[e]), int(ev[e])
+        sc = [eva_exact(u, v, i, d_rep, h_rep, host, e_count, v_count, len(eu), n, p,
+                        alpha=Fraction(*cfg.alpha), beta=Fraction(*cfg.beta),
+                        gamma=Fraction(*cfg.gamma)) for i in range(p)]
+        best = min(range(p), key=lambda i: (sc[i], i))
+        out[e] = best
+        e_count[best] += 1
+        for x in (u, v):
+            if best not in d_rep[x]:
+                v_count[best] += 1
+                d_rep[x].add(best)
+                if first[x] is None:
+                    first[x] = best
+            h_rep[x].add(host[best])
+    return out, first
+
+
+@pytest.mark.parametrize("seed,p,hosts,order", [(1, 2, 1, "degsum"), (2, 3, 1, "input"),
+                                                (3, 4, 2, "degsum"), (4, 4, 2, "shuffle"),
+                                                (5, 3, 3, "input")])
+def test_brute_force_greedy(seed, p, hosts, order):
+    d = small_random_graph(9, 12, (2, 2), seed=seed)
+    cfg = PartitionCfg(p=p, num_hosts=hosts, edge_order=order, seed=seed)
+    ep, ms = ebv_partition(d.n, d.eu, d.ev, cfg)
+    ref, first = _brute_greedy(d.n, d.eu, d.ev, cfg)
+    assert ep.tolist() == ref
+    for x in range(d.n):
+        if first[x] is not None:
+            assert ms[x] == first[x]
+
+
+def test_integer_scores_match_equation_on_random_states():
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        p = int(rng.integers(1, 6))
+        n = int(rng.integers(2, 10))
+        E = int(rng.integers(1, 50))
+        hosts = int(rng.integers(1, p + 1))
+        host = [i * hosts // p for i in range(p)]
+        gn, gd = int(rng.integers(0, 5)), int(rng.integers(5, 11))
+        an, ad = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+        bn, bd = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+        d_rep = [set(np.flatnonzero(rng.random(p) < 0.4).tolist()) for _ in range(n)]
+        h_rep = [{host[i] for i in s} for s in d_rep]
+        e_count = rng.integers(0, 20, size=p).tolist()
+        v_count = rng.integers(0, 20, size=p).tolist()
+        u, v = 0, 1
+        K = gd * ad * bd * E * n
+        for i in range(p):
+            ex = eva_exact(u, v, i, d_rep, h_rep, host, e_count, v_count, E, n, p,
+                           alpha=Fraction(an, ad), beta=Fraction(bn, bd), gamma=Fraction(gn, gd))
+            rep = int(i not in d_rep[u]) + int(i not in d_rep[v])
+            hst = int(host[i] not in h_rep[u]) + int(host[i] not in h_rep[v])
+            s = ((gd - gn) * ad * bd * E * n * rep + gn * ad * bd * E * n * hst
+                 + an * gd * bd * p * e_count[i] * n + bn * gd * ad * p * v_count[i] * E)
+            assert ex * K == s
+
+
+def test_single_part_degeneracy():
+    d = small_random_graph(200, 600, (4, 3), seed=9)
+    plan = partition(d.n, d.eu, d.ev, PartitionCfg(p=1))
+    st = stats(plan)
+    assert st.rf == 1.0 and st.edge_if == 1.0 and st.vertex_if == 1.0
+    assert st.inner_max == 0 and st.outer_max == 0 and st.total_mirrors == 0
+    assert plan.parts[0].n_mirror == 0 and plan.parts[0].n_bmaster == 0
+
+
+def test_two_hosts_one_gpu_each_gamma_invariant():
+    """with 2 GPUs (one per host) EBV γ=0.1 and γ=0 give the same partition."""
+    for seed in range(3):
+        d = small_random_graph(300, 1200, (4, 3), seed=20 + seed)
+        a = ebv_partition(d.n, d.eu, d.ev, PartitionCfg(p=2, num_hosts=2, gamma=(1, 10)))
+        b = ebv_partition(d.n, d.eu, d.ev, PartitionCfg(p=2, num_hosts=2, gamma=(0, 10)))
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_table3_mean_outer_reduction():
+    t = golden("table3.json")
+    red = [outer_reduction(r["gamma0"]["outer"], r["gamma01"]["outer"]) for r in t["rows"]]
+    assert abs(100 * np.mean(red) - t["claimed_mean_outer_reduction_pct"]) < 0.005
+
+
+@pytest.mark.parametrize("p,hosts", [(2, 1), (3, 1), (4, 2), (8, 1)])
+def test_plan_invariants(p, hosts):
+    d = small_random_graph(400, 1500, (4, 3), seed=11 + p)
+    cfg = PartitionCfg(p=p, num_hosts=hosts)
+    plan = partition(d.n, d.eu, d.ev, cfg)
+    # every edge assigned once; masters unique and a replica
+    assert sum(pp.n_edges for pp in plan.parts) == d.m
+    # replica sets by explicit count from the edge assignment
+    reps = [set() for _ in range(d.n)]
+    for e in range(d.m):
+        reps[int(d.eu[e])].add(int(plan.edge_part[e]))
+        reps[int(d.ev[e])].add(int(plan.edge_part[e]))
+    for x in range(d.n):
+        reps[x].add(int(plan.master[x]))
+    st = stats(plan)
+    assert st.sum_vi == sum(len(r) for r in reps)
+    assert abs(st.rf - sum(len(r) for r in reps) / d.n) < 1e-15
+    assert st.total_mirrors == sum(len(r) - 1 for r in reps)
+    for pp in plan.parts:
+        i = pp.part
+        l2g = pp.local2global.tolist()
+        assert sorted(l2g) == sorted(x for x in range(d.n) if i in reps[x])
+        B, M = pp.n_bmaster, pp.n_mirror
+        bm = l2g[:B]
+        assert bm == sorted(x for x in range(d.n) if plan.master[x] == i and len(reps[x]) >= 2)
+        inter = l2g[B + M:]
+        assert inter == sorted(x for x in range(d.n) if plan.master[x] == i and len(reps[x]) == 1)
+        for j in range(p):
+            slab = l2g[B + pp.mirror_off[j]:B + pp.mirror_off[j + 1]]
+            assert slab == sorted(x for x in range(d.n) if plan.master[x] == j and j != i
+                                  and i in reps[x])
+            if j != i:
+                # master side lists point at the same vertices, same order
+                mside = plan.parts[j].local2global[plan.parts[j].halo_master[i]].tolist()
+                assert mside == slab
+    # the parts' adjacencies add up to the whole graph's Â
+    A = normalized_adjacency(d.n, d.eu, d.ev)
+    S = sp.csr_matrix((d.n, d.n))
+    for pp in plan.parts:
+        Ai = sp.csr_matrix((pp.val64, pp.colidx, pp.rowptr), shape=(pp.n_local, pp.n_local)).tocoo()
+        g = pp.local2global
+        S = S + sp.csr_matrix((Ai.data, (g[Ai.row], g[Ai.col])), shape=(d.n, d.n))
+    assert abs(S - A).max() == 0
+    # Table 3 inner/outer: every (i, j) halo list is one gather + one scatter stream
+    host = cfg.hosts()
+    inner = [0] * p
+    outer = [0] * p
+    for x in range(d.n):
+        for i in reps[x]:
+            if i != plan.master[x]:
+                same = host[i] == host[plan.master[x]]
+                for k in (i, plan.master[x]):
+                    (inner if same else outer)[k] += 1
+    assert st.inner_max == max(inner) and st.outer_max == max(outer)
+
+
+def test_edge_imbalance_small():
+    d = small_random_graph(2000, 8000, (4, 3), seed=33)
+    st = stats(partition(d.n, d.eu, d.ev, PartitionCfg(p=4)))
+    assert st.edge_if < 1.05 and st.vertex_if < 1.05
