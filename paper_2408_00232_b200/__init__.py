@@ -1,0 +1,35 @@
+"""B200-native CDFGNN hot path (arXiv 2408.00232): partitioner + per-layer
+distributed full-batch GCN step behind the C ABI of include/cdfgnn.h.
+
+The functions below carry the C names (without the ``cdfgnn_`` prefix) and only
+marshal arguments; every step of the path runs in libcdfgnn.so (host C++
+partitioner, sm_100a kernels, NCCL).  ``runtime.Run`` wires a synthetic
+dataset, torch device memory and a process group to them.
+"""
+from .api import (  # noqa: F401
+    Plan,
+    Ctx,
+    CdfgnnError,
+    partition,
+    plan_part,
+    plan_stats,
+    cfg_default,
+    get_unique_id,
+    workspace_size,
+    init,
+    destroy,
+    halo_exchange,
+    layer_fwd,
+    layer_bwd,
+    epoch,
+    epoch_host,
+    cache_view,
+    sync_flags,
+    reset_caches,
+    get_eps,
+    set_eps,
+    spmm,
+    last_error,
+    version,
+    ld_of,
+)

@@ -1,0 +1,935 @@
+// libcdfgnn C ABI: context, workspace carving, halo exchange orchestration,
+// layer forward/backward and the Alg. 1 epoch.
+//
+// Transport: co-resident partitions (world == 1, k == p parts on one GPU) read
+// each other's message regions directly in device memory; one partition per GPU
+// (world == p) exchanges message counts and then payloads with grouped NCCL
+// send/recv over NVLink (§3.2 gather / scatter), and sums weight
+// gradients with ncclAllReduce (the "parameter server" of P:L221-222, reading R9).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "kernels.h"
+
+namespace cdfgnn {
+
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+}  // namespace cdfgnn
+
+using namespace cdfgnn;
+
+#define CUDA_TRY(x)                                                                         \
+    do {                                                                                    \
+        cudaError_t _e = (x);                                                               \
+        if (_e != cudaSuccess) CDF_FAIL(CDFGNN_ECUDA, "%s: %s", #x, cudaGetErrorString(_e)); \
+    } while (0)
+#define NCCL_TRY(x)                                                                         \
+    do {                                                                                    \
+        ncclResult_t _r = (x);                                                              \
+        if (_r != ncclSuccess) CDF_FAIL(CDFGNN_ENCCL, "%s: %s", #x, ncclGetErrorString(_r)); \
+    } while (0)
+
+namespace {
+
+struct Bump {
+    uint8_t* base = nullptr;
+    size_t off = 0;
+    template <class T>
+    T* take(int64_t count, size_t align = 256) {
+        off = (off + align - 1) / align * align;
+        T* p = reinterpret_cast<T*>(base + off);
+        off += (size_t)std::max<int64_t>(count, 0) * sizeof(T);
+        return p;
+    }
+};
+
+enum Phase { PH_GEMM = 0, PH_SPMM = 1, PH_SYNC = 2, PH_OTHER = 3, PH_END = 4 };
+
+struct LocalPart {
+    int32_t part = 0;
+    int64_t n = 0, B = 0, M = 0, nnz = 0;
+    const int32_t* rowptr_h = nullptr;
+    const int32_t* colidx_h = nullptr;
+    const float* val_h = nullptr;
+    const int32_t* halo_h = nullptr;
+    std::vector<int64_t> moff, hoff;
+    std::vector<int64_t> capA, capB;   // region capacities per peer
+    // device
+    int32_t *rowptr = nullptr, *colidx = nullptr, *halo_local = nullptr;
+    float* val = nullptr;
+    int64_t *moff_d = nullptr, *hoff_d = nullptr;
+    uint8_t* regA[kMaxParts] = {};
+    uint8_t* regB[kMaxParts] = {};
+    RegionTab *gsend_d = nullptr, *grecv_d = nullptr, *ssend_d = nullptr, *srecv_d = nullptr;
+    RegionTab gsend_h{}, grecv_h{}, ssend_h{}, srecv_h{};
+    int32_t* cnt = nullptr;           // [4p]: gsend | grecv | ssend | srecv
+    int32_t* cnt_h = nullptr;         // pinned
+    uint8_t *gflag = nullptr, *fired = nullptr, *active = nullptr;
+    int32_t *idxmap = nullptr, *mmap = nullptr;
+    uint8_t* stage_codes = nullptr;
+    float *stage_lohi = nullptr, *stage_a = nullptr;
+    unsigned long long *status_g = nullptr, *status_s = nullptr, *ticket = nullptr;
+    unsigned long long tbase_g = 0, tbase_s = 0;
+    uint32_t seq = 0;
+    CacheDev cache[CDFGNN_MAX_LAYERS][2] = {};
+    float* act[CDFGNN_MAX_LAYERS + 1] = {};
+    float *T = nullptr, *S = nullptr, *D[2] = {nullptr, nullptr}, *rowloss = nullptr;
+    float* X_stage = nullptr;
+    int32_t* lab_stage = nullptr;
+    uint8_t* mask_stage = nullptr;
+    HaloDev halo{};
+};
+
+}  // namespace
+
+struct cdfgnn_ctx {
+    cdfgnn_cfg cfg{};
+    int32_t p = 0, k = 0, rank = 0, world = 1, device = 0;
+    std::vector<LocalPart> parts;
+    ncclComm_t comm = nullptr;
+    int64_t Fmax = 0, ldmax = 0, hdr_bytes = 4, wtotal = 0;
+    int64_t woff[CDFGNN_MAX_LAYERS + 1] = {};
+    int64_t splitk_cap = 0;
+    float *dW = nullptr, *adam_m = nullptr, *adam_v = nullptr, *splitk = nullptr;
+    unsigned long long* stats_d = nullptr;    // [L][2][4]
+    unsigned long long* stats_h = nullptr;    // pinned
+    double* loss_d = nullptr;        // [k]
+    int32_t* scal_d = nullptr;       // [0] correct, [1] err, [2] ntrain
+    double* host_scratch = nullptr;  // pinned: k doubles + ints
+    int64_t ntrain = -1;
+    double eps = 0.01, mean_acc = 0.0;
+    bool have_mean = false;
+    int64_t step_t = 0;
+    int launches = 0;
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> ev_phase;
+    size_t ev_used = 0;
+    size_t ws_bytes = 0;
+    void* ws = nullptr;
+};
+
+namespace {
+
+int64_t sync_width(const cdfgnn_ctx* c, int l) { return c->cfg.dims[l]; }
+
+// host-side sizes from the plan
+int prepare(cdfgnn_ctx* c, const cdfgnn_plan* plan, const int32_t* parts, int32_t k,
+            const cdfgnn_cfg* cfg) {
+    if (!plan || !cfg) CDF_FAIL(CDFGNN_EUSAGE, "plan/cfg is NULL");
+    c->cfg = *cfg;
+    c->p = cdfgnn_plan_num_parts(plan);
+    c->k = k;
+    if (cfg->L < 1 || cfg->L > CDFGNN_MAX_LAYERS) CDF_FAIL(CDFGNN_EUSAGE, "L must be in [1, %d]", CDFGNN_MAX_LAYERS);
+    if (cfg->quant_bits != 0 && cfg->quant_bits != 8) CDF_FAIL(CDFGNN_EUSAGE, "quant_bits must be 0 or 8");
+    for (int l = 0; l <= cfg->L; ++l)
+        if (cfg->dims[l] < 1) CDF_FAIL(CDFGNN_EUSAGE, "dims[%d] must be >= 1", l);
+    for (int l = 1; l <= cfg->L; ++l)
+        if (cfg->dims[l] > 1024) CDF_FAIL(CDFGNN_EUSAGE, "hidden/output widths must be <= 1024");
+    if (cfg->dims[cfg->L] > 256) CDF_FAIL(CDFGNN_EUSAGE, "at most 256 classes");
+    if (k < 1 || k > c->p) CDF_FAIL(CDFGNN_EUSAGE, "k must be in [1, p]");
+    c->Fmax = 0;
+    for (int l = 1; l <= cfg->L; ++l) c->Fmax = std::max<int64_t>(c->Fmax, cfg->dims[l]);
+    c->ldmax = ld_of(c->Fmax);
+    c->hdr_bytes = cfg->quant_bits ? 12 : 4;
+    c->wtotal = 0;
+    for (int l = 1; l <= cfg->L; ++l) {
+        c->woff[l - 1] = c->wtotal;
+        c->wtotal += (int64_t)cfg->dims[l - 1] * cfg->dims[l];
+    }
+    c->woff[cfg->L] = c->wtotal;
+    int64_t maxw = 0;
+    for (int l = 1; l <= cfg->L; ++l) maxw = std::max<int64_t>(maxw, (int64_t)cfg->dims[l - 1] * cfg->dims[l]);
+    c->splitk_cap = 64 * maxw;
+    c->parts.assign(k, LocalPart());
+    for (int t = 0; t < k; ++t) {
+        cdfgnn_part_view v;
+        CDF_TRY(cdfgnn_plan_part(plan, parts[t], &v));
+        LocalPart& P = c->parts[t];
+        P.part = parts[t];
+        P.n = v.n_local; P.B = v.n_bmaster; P.M = v.n_mirror; P.nnz = v.nnz;
+        P.rowptr_h = v.rowptr; P.colidx_h = v.colidx; P.val_h = v.val; P.halo_h = v.halo_local;
+        P.moff.assign(v.mirror_off, v.mirror_off + c->p + 1);
+        P.hoff.assign(v.halo_off, v.halo_off + c->p + 1);
+        P.capA.resize(c->p); P.capB.resize(c->p);
+        for (int j = 0; j < c->p; ++j) {
+            P.capA[j] = P.moff[j + 1] - P.moff[j];
+            P.capB[j] = P.hoff[j + 1] - P.hoff[j];
+        }
+    }
+    return CDFGNN_OK;
+}
+
+int64_t region_bytes(const cdfgnn_ctx* c, int64_t cap) {
+    const int64_t rowb = c->cfg.quant_bits ? c->Fmax : 4 * c->ldmax;
+    return align_up(cap * c->hdr_bytes, 256) + cap * rowb;
+}
+
+void carve(cdfgnn_ctx* c, Bump& b) {
+    const int p = c->p, L = c->cfg.L;
+    for (LocalPart& P : c->parts) {
+        P.rowptr = b.take<int32_t>(P.n + 1);
+        P.colidx = b.take<int32_t>(P.nnz);
+        P.val = b.take<float>(P.nnz);
+        P.halo_local = b.take<int32_t>(P.hoff[p]);
+        P.moff_d = b.take<int64_t>(p + 1);
+        P.hoff_d = b.take<int64_t>(p + 1);
+        for (int j = 0; j < p; ++j) {
+            P.regA[j] = b.take<uint8_t>(region_bytes(c, P.capA[j]));
+            P.regB[j] = b.take<uint8_t>(region_bytes(c, P.capB[j]));
+        }
+        P.gsend_d = b.take<RegionTab>(1);
+        P.grecv_d = b.take<RegionTab>(1);
+        P.ssend_d = b.take<RegionTab>(1);
+        P.srecv_d = b.take<RegionTab>(1);
+        P.cnt = b.take<int32_t>(4 * p);
+        P.gflag = b.take<uint8_t>(P.M);
+        P.fired = b.take<uint8_t>(P.B);
+        P.active = b.take<uint8_t>(P.B);
+        P.idxmap = b.take<int32_t>((int64_t)p * P.B);
+        P.mmap = b.take<int32_t>(P.M);
+        P.stage_codes = b.take<uint8_t>(P.B * c->Fmax);
+        P.stage_lohi = b.take<float>(2 * P.B);
+        P.stage_a = b.take<float>(P.B * c->ldmax);
+        int64_t tg = 0;
+        for (int j = 0; j < p; ++j) tg += (P.capA[j] + 7) / 8;
+        P.status_g = b.take<unsigned long long>(tg + 1);
+        P.status_s = b.take<unsigned long long>(scatter_tiles_host(P.hoff.data(), p) + 1);
+        P.ticket = b.take<unsigned long long>(2);
+        for (int l = 1; l <= L; ++l) {
+            const int64_t ld = ld_of(c->cfg.dims[l]);
+            for (int dir = 0; dir < 2; ++dir) {
+                CacheDev& cd = P.cache[l - 1][dir];
+                if (c->cfg.cache_on) {
+                    cd.s_mir = b.take<float>(P.M * ld);
+                    cd.b_mir = b.take<float>(P.M * ld);
+                    cd.s_mas = b.take<float>(P.B * ld);
+                    cd.a = b.take<float>(P.B * ld);
+                    cd.b_mas = b.take<float>(P.B * ld);
+                } else {
+                    cd = CacheDev{};
+                }
+            }
+            P.act[l] = b.take<float>(P.n * ld);
+        }
+        P.T = b.take<float>(P.n * c->ldmax);
+        P.S = b.take<float>(P.n * c->ldmax);
+        P.D[0] = b.take<float>(P.n * c->ldmax);
+        P.D[1] = b.take<float>(P.n * c->ldmax);
+        P.rowloss = b.take<float>(P.n);
+        P.X_stage = b.take<float>(P.n * ld_of(c->cfg.dims[0]));
+        P.lab_stage = b.take<int32_t>(P.n);
+        P.mask_stage = b.take<uint8_t>(P.n);
+    }
+    c->dW = b.take<float>(c->wtotal);
+    c->adam_m = b.take<float>(c->wtotal);
+    c->adam_v = b.take<float>(c->wtotal);
+    c->splitk = b.take<float>(c->splitk_cap);
+    c->stats_d = b.take<unsigned long long>(CDFGNN_MAX_LAYERS * 2 * 4);
+    c->loss_d = b.take<double>(std::max(c->k, 1));
+    c->scal_d = b.take<int32_t>(8);
+}
+
+// ---- phase timing ----------------------------------------------------------------
+void mark(cdfgnn_ctx* c, int phase, cudaStream_t s) {
+    if (!c->timing) return;
+    if (c->ev_used >= c->ev.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        c->ev.push_back(e);
+        c->ev_phase.push_back(0);
+    }
+    cudaEventRecord(c->ev[c->ev_used], s);
+    c->ev_phase[c->ev_used] = phase;
+    c->ev_used++;
+}
+
+void build_tables(cdfgnn_ctx* c) {
+    const int p = c->p;
+    for (int t = 0; t < c->k; ++t) {
+        LocalPart& P = c->parts[t];
+        int32_t* cg_send = P.cnt;
+        int32_t* cg_recv = P.cnt + p;
+        int32_t* cs_send = P.cnt + 2 * p;
+        int32_t* cs_recv = P.cnt + 3 * p;
+        for (int j = 0; j < p; ++j) {
+            P.gsend_h.hdr[j] = P.regA[j];
+            P.gsend_h.pay[j] = P.regA[j] + align_up(P.capA[j] * c->hdr_bytes, 256);
+            P.gsend_h.cnt[j] = cg_send + j;
+            P.ssend_h.hdr[j] = P.regB[j];
+            P.ssend_h.pay[j] = P.regB[j] + align_up(P.capB[j] * c->hdr_bytes, 256);
+            P.ssend_h.cnt[j] = cs_send + j;
+        }
+    }
+    for (int t = 0; t < c->k; ++t) {
+        LocalPart& P = c->parts[t];
+        const int me = P.part;
+        for (int s = 0; s < p; ++s) {
+            if (c->world == 1) {
+                // co-resident partitions: read the sender's region in place
+                LocalPart& Q = c->parts[s];
+                P.grecv_h.hdr[s] = Q.gsend_h.hdr[me];
+                P.grecv_h.pay[s] = Q.gsend_h.pay[me];
+                P.grecv_h.cnt[s] = Q.gsend_h.cnt[me];
+                P.srecv_h.hdr[s] = Q.ssend_h.hdr[me];
+                P.srecv_h.pay[s] = Q.ssend_h.pay[me];
+                P.srecv_h.cnt[s] = Q.ssend_h.cnt[me];
+            } else {
+                P.grecv_h.hdr[s] = P.regB[s];
+                P.grecv_h.pay[s] = P.ssend_h.pay[s];
+                P.grecv_h.cnt[s] = P.cnt + p + s;
+                P.srecv_h.hdr[s] = P.regA[s];
+                P.srecv_h.pay[s] = P.gsend_h.pay[s];
+                P.srecv_h.cnt[s] = P.cnt + 3 * p + s;
+            }
+        }
+        HaloDev& h = P.halo;
+        h.me = me; h.p = p; h.n = P.n; h.B = P.B; h.M = P.M;
+        h.quant = c->cfg.quant_bits; h.hdr_bytes = c->hdr_bytes;
+        h.moff = P.moff_d; h.hoff = P.hoff_d; h.halo_local = P.halo_local;
+        h.gsend = P.gsend_d; h.grecv = P.grecv_d; h.ssend = P.ssend_d; h.srecv = P.srecv_d;
+        h.cnt_gsend = P.cnt; h.cnt_ssend = P.cnt + 2 * p;
+        h.gflag = P.gflag; h.fired = P.fired; h.active = P.active;
+        h.idxmap = P.idxmap; h.mmap = P.mmap;
+        h.stage_codes = P.stage_codes; h.stage_lohi = P.stage_lohi; h.stage_a = P.stage_a;
+        h.status_g = P.status_g; h.status_s = P.status_s; h.ticket = P.ticket;
+        h.err = c->scal_d + 1;
+    }
+}
+
+int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) CDF_FAIL(CDFGNN_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+    return CDFGNN_OK;
+}
+
+// NCCL count + payload exchange for one phase (world > 1, k == 1)
+int nccl_phase(cdfgnn_ctx* c, LocalPart& P, bool gather, int64_t rowb, cudaStream_t s,
+               int64_t* wire) {
+    const int p = c->p, me = P.part;
+    int32_t* snd = gather ? P.cnt : P.cnt + 2 * p;
+    int32_t* rcv = gather ? P.cnt + p : P.cnt + 3 * p;
+    NCCL_TRY(ncclGroupStart());
+    for (int j = 0; j < p; ++j) {
+        if (j == me) continue;
+        NCCL_TRY(ncclSend(snd + j, 1, ncclInt32, j, c->comm, s));
+        NCCL_TRY(ncclRecv(rcv + j, 1, ncclInt32, j, c->comm, s));
+    }
+    NCCL_TRY(ncclGroupEnd());
+    CUDA_TRY(cudaMemcpyAsync(P.cnt_h, P.cnt, sizeof(int32_t) * 4 * p, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    const int32_t* hs = P.cnt_h + (gather ? 0 : 2 * p);
+    const int32_t* hr = P.cnt_h + (gather ? p : 3 * p);
+    const RegionTab& st = gather ? P.gsend_h : P.ssend_h;
+    const RegionTab& rt = gather ? P.grecv_h : P.srecv_h;
+    const std::vector<int64_t>& scap = gather ? P.capA : P.capB;
+    const std::vector<int64_t>& rcap = gather ? P.capB : P.capA;
+    for (int j = 0; j < p; ++j) {
+        if (j == me) continue;
+        if (hs[j] < 0 || hs[j] > scap[j] || hr[j] < 0 || hr[j] > rcap[j])
+            CDF_FAIL(CDFGNN_EPROTO, "message count out of range (peer %d: send %d/%lld recv %d/%lld)",
+                     j, hs[j], (long long)scap[j], hr[j], (long long)rcap[j]);
+    }
+    NCCL_TRY(ncclGroupStart());
+    for (int j = 0; j < p; ++j) {
+        if (j == me) continue;
+        if (hs[j] > 0) {
+            NCCL_TRY(ncclSend(st.hdr[j], (size_t)hs[j] * c->hdr_bytes, ncclUint8, j, c->comm, s));
+            NCCL_TRY(ncclSend(st.pay[j], (size_t)hs[j] * rowb, ncclUint8, j, c->comm, s));
+            *wire += (int64_t)hs[j] * (c->hdr_bytes + rowb);
+        }
+        if (hr[j] > 0) {
+            NCCL_TRY(ncclRecv(rt.hdr[j], (size_t)hr[j] * c->hdr_bytes, ncclUint8, j, c->comm, s));
+            NCCL_TRY(ncclRecv(rt.pay[j], (size_t)hr[j] * rowb, ncclUint8, j, c->comm, s));
+        }
+    }
+    NCCL_TRY(ncclGroupEnd());
+    return CDFGNN_OK;
+}
+
+int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float eps,
+              cudaStream_t s, int64_t* wire) {
+    const int p = c->p;
+    const int F = (int)sync_width(c, l);
+    if (ld != ld_of(F)) CDF_FAIL(CDFGNN_EUSAGE, "ld %lld must equal roundup(F=%d, 4)", (long long)ld, F);
+    mark(c, PH_SYNC, s);
+    std::vector<SyncArgs> args(c->k);
+    for (int t = 0; t < c->k; ++t) {
+        LocalPart& P = c->parts[t];
+        SyncArgs& a = args[t];
+        a.X = X[t]; a.ld = ld; a.F = F; a.eps = eps;
+        a.nocache = c->cfg.cache_on ? 0 : 1;
+        a.c = P.cache[l - 1][dir];
+        a.stats = c->stats_d + ((l - 1) * 2 + dir) * 4;
+        a.seq = ++P.seq;
+    }
+    const int64_t rowb = c->cfg.quant_bits ? F : 4 * ld;
+    // ---- gather: mirrors test, quantise, pack (Alg. 2 L3-L9)
+    for (int t = 0; t < c->k; ++t) {
+        LocalPart& P = c->parts[t];
+        CUDA_TRY(cudaMemsetAsync(P.cnt, 0, sizeof(int32_t) * p, s));
+        const int nt = gather_tiles_host(P.moff.data(), p, ld);
+        args[t].ticket_base_g = P.tbase_g;
+        c->launches += launch_gather_pack_n(P.halo, args[t], nt, s);
+        P.tbase_g += nt;
+    }
+    CDF_TRY(check_launch("gather_pack"));
+    if (c->world > 1) CDF_TRY(nccl_phase(c, c->parts[0], true, rowb, s, wire));
+    // ---- masters: apply in ascending source order, own test, stage scatter (L10-L19)
+    for (int t = 0; t < c->k; ++t) {
+        LocalPart& P = c->parts[t];
+        if (P.B == 0) continue;
+        CUDA_TRY(cudaMemsetAsync(P.idxmap, 0xFF, sizeof(int32_t) * p * P.B, s));
+        c->launches += launch_map(P.halo, 0, *std::max_element(P.capB.begin(), P.capB.end()), s);
+        c->launches += launch_master(P.halo, args[t], s);
+    }
+    CDF_TRY(check_launch("master"));
+    // ---- scatter: active masters to every mirror (L20-L22)
+    for (int t = 0; t < c->k; ++t) {
+        LocalPart& P = c->parts[t];
+        CUDA_TRY(cudaMemsetAsync(P.cnt + 2 * p, 0, sizeof(int32_t) * p, s));
+        const int nt = scatter_tiles_host(P.hoff.data(), p);
+        args[t].ticket_base_s = P.tbase_s;
+        c->launches += launch_scatter_pack_n(P.halo, args[t], nt, s);
+        P.tbase_s += nt;
+    }
+    CDF_TRY(check_launch("scatter_pack"));
+    if (c->world > 1) CDF_TRY(nccl_phase(c, c->parts[0], false, rowb, s, wire));
+    for (int t = 0; t < c->k; ++t) {
+        LocalPart& P = c->parts[t];
+        if (P.M == 0) continue;
+        CUDA_TRY(cudaMemsetAsync(P.mmap, 0xFF, sizeof(int32_t) * P.M, s));
+        c->launches += launch_map(P.halo, 1, *std::max_element(P.capA.begin(), P.capA.end()), s);
+        c->launches += launch_mirror_apply(P.halo, args[t], s);
+    }
+    CDF_TRY(check_launch("mirror_apply"));
+    return CDFGNN_OK;
+}
+
+void fill_sync_stats(const cdfgnn_ctx* c, int l, int dir, const unsigned long long* h, int64_t wire,
+                     cdfgnn_sync_stats* st) {
+    const int64_t F = sync_width(c, l);
+    st->gather_sent = h[0];
+    st->master_fired = h[1];
+    st->active = h[2];
+    st->scatter_msgs = h[3];
+    int64_t M = 0;
+    for (const LocalPart& P : c->parts) M += P.M;
+    st->baseline = 2 * M;
+    const int64_t mb = c->cfg.quant_bits ? F + 12 : 4 * F + 4;
+    st->bytes_alg = (h[0] + h[3]) * mb;
+    st->bytes_wire = wire;
+    (void)dir;
+}
+
+int read_stats_now(cdfgnn_ctx* c, int l, int dir, int64_t wire, cudaStream_t s,
+                   cdfgnn_sync_stats* st) {
+    unsigned long long* slot = c->stats_d + ((l - 1) * 2 + dir) * 4;
+    CUDA_TRY(cudaMemcpyAsync(c->stats_h, slot, sizeof(long long) * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    fill_sync_stats(c, l, dir, c->stats_h, wire, st);
+    return CDFGNN_OK;
+}
+
+int spmm_part(cdfgnn_ctx* c, LocalPart& P, const float* T, float* Y, int64_t ld, cudaStream_t s) {
+    mark(c, PH_SPMM, s);
+    launch_spmm(P.rowptr, P.colidx, P.val, P.n, T, Y, ld, s);
+    c->launches++;
+    return check_launch("spmm");
+}
+
+int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, const float* W,
+             float* const* Z, float* const* H_out, int64_t ld_out, float eps, cudaStream_t s,
+             int64_t* wire) {
+    const int64_t Fi = c->cfg.dims[l - 1], Fo = c->cfg.dims[l];
+    if (ld_in < Fi || ld_in % 4 || ld_out != ld_of(Fo)) CDF_FAIL(CDFGNN_EUSAGE, "bad leading dimension");
+    for (int t = 0; t < c->k; ++t) {
+        LocalPart& P = c->parts[t];
+        mark(c, PH_GEMM, s);
+        launch_gemm_simt(false, false, P.n, Fo, Fi, H_in[t], ld_in, W, Fo, P.T, ld_out, nullptr, 0,
+                         nullptr, 0, false, s);
+        c->launches++;
+        CDF_TRY(check_launch("gemm fwd"));
+        CDF_TRY(spmm_part(c, P, P.T, Z[t], ld_out, s));
+    }
+    CDF_TRY(halo_impl(c, l, 0, Z, ld_out, eps, s, wire));
+    if (H_out) {
+        mark(c, PH_OTHER, s);
+        for (int t = 0; t < c->k; ++t) {
+            launch_relu(Z[t], H_out[t], c->parts[t].n * ld_out, s);
+            c->launches++;
+        }
+        CDF_TRY(check_launch("relu"));
+    }
+    return CDFGNN_OK;
+}
+
+int bwd_impl(cdfgnn_ctx* c, int l, float* const* dZ, int64_t ld, const float* const* H_in,
+             int64_t ld_in, const float* W, float* const* dZ_prev, float* dW, float eps,
+             cudaStream_t s, int64_t* wire) {
+    const int64_t Fi = c->cfg.dims[l - 1], Fo = c->cfg.dims[l];
+    if (ld != ld_of(Fo) || ld_in < Fi || ld_in % 4) CDF_FAIL(CDFGNN_EUSAGE, "bad leading dimension");
+    CDF_TRY(halo_impl(c, l, 1, dZ, ld, eps, s, wire));
+    for (int t = 0; t < c->k; ++t) {
+        LocalPart& P = c->parts[t];
+        CDF_TRY(spmm_part(c, P, dZ[t], P.S, ld, s));
+        mark(c, PH_GEMM, s);
+        // dW (+)= H_inᵀ S ; parts accumulate in ascending order
+        launch_gemm_simt(true, false, Fi, Fo, P.n, H_in[t], ld_in, P.S, ld, dW, Fo, nullptr, 0,
+                         c->splitk, c->splitk_cap, t > 0, s);
+        c->launches += 2;
+        if (dZ_prev) {
+            launch_gemm_simt(false, true, P.n, Fi, Fo, P.S, ld, W, Fo, dZ_prev[t], ld_in, H_in[t],
+                             ld_in, nullptr, 0, false, s);
+            c->launches++;
+        }
+        CDF_TRY(check_launch("gemm bwd"));
+    }
+    return CDFGNN_OK;
+}
+
+double update_eps(const cdfgnn_cfg& g, double eps, double acc, double mean) {
+    // P:L387-393, literal, then the R17 clamp
+    if (acc < mean - g.mu1 && eps < g.nu1) eps = std::min(g.lam1 * eps, eps + g.xi);
+    else if (acc > mean + g.mu2 && eps > g.nu2) eps = std::max(g.lam2 * eps, eps - g.xi);
+    if (g.eps_clamp) eps = std::min(std::max(eps, g.nu2), g.nu1);
+    return eps;
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" int cdfgnn_cfg_default(cdfgnn_cfg* cfg) {
+    if (!cfg) CDF_FAIL(CDFGNN_EUSAGE, "cfg is NULL");
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->L = 2;
+    cfg->dims[0] = 16; cfg->dims[1] = 16; cfg->dims[2] = 7;
+    cfg->cache_on = 1;
+    cfg->eps_init = 0.01;
+    cfg->adaptive = 1;
+    cfg->mu1 = 0.001; cfg->mu2 = 0.02; cfg->nu1 = 0.3; cfg->nu2 = 0.001;
+    cfg->xi = 0.01; cfg->lam1 = 1.05; cfg->lam2 = 0.9;
+    cfg->eps_clamp = 1;
+    cfg->quant_bits = 8;
+    cfg->optimizer = 1;
+    cfg->lr = 0.01; cfg->beta1 = 0.9; cfg->beta2 = 0.999; cfg->adam_eps = 1e-8;
+    cfg->gemm_tf32 = 0;
+    cfg->timing = 0;
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_get_unique_id(void* out128) {
+    if (!out128) CDF_FAIL(CDFGNN_EUSAGE, "out is NULL");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+    ncclUniqueId id;
+    NCCL_TRY(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_workspace_size(const cdfgnn_plan* plan, const int32_t* parts, int32_t k,
+                                     const cdfgnn_cfg* cfg, size_t* bytes) {
+    if (!bytes || !parts) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+    cdfgnn_ctx c;
+    CDF_TRY(prepare(&c, plan, parts, k, cfg));
+    Bump b;
+    carve(&c, b);
+    *bytes = align_up((int64_t)b.off, 256);
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_init(const cdfgnn_plan* plan, const int32_t* parts, int32_t k, int32_t rank,
+                           int32_t world, const void* nccl_uid, int32_t device, void* workspace,
+                           size_t workspace_bytes, const cdfgnn_cfg* cfg, cdfgnn_ctx** out) {
+    if (!out || !parts || !workspace) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+    *out = nullptr;
+    if (((uintptr_t)workspace) % 256) CDF_FAIL(CDFGNN_EUSAGE, "workspace must be 256-byte aligned");
+    std::unique_ptr<cdfgnn_ctx> c(new cdfgnn_ctx());
+    CDF_TRY(prepare(c.get(), plan, parts, k, cfg));
+    if (world < 1 || rank < 0 || rank >= world) CDF_FAIL(CDFGNN_EUSAGE, "bad rank/world");
+    if (world == 1) {
+        if (k != c->p) CDF_FAIL(CDFGNN_EUSAGE, "world == 1 requires all %d parts local (k = %d)", c->p, k);
+        for (int t = 0; t < k; ++t)
+            if (parts[t] != t) CDF_FAIL(CDFGNN_EUSAGE, "parts must be 0..p-1 in order");
+    } else {
+        if (k != 1 || world != c->p || parts[0] != rank)
+            CDF_FAIL(CDFGNN_EUSAGE, "world > 1 requires one partition per rank (part == rank, p == world)");
+        if (!nccl_uid) CDF_FAIL(CDFGNN_EUSAGE, "nccl_uid required for world > 1");
+    }
+    c->rank = rank; c->world = world; c->device = device;
+    Bump b;
+    carve(c.get(), b);
+    const size_t need = align_up((int64_t)b.off, 256);
+    if (workspace_bytes < need)
+        CDF_FAIL(CDFGNN_EWORKSPACE, "workspace too small: %zu < %zu", workspace_bytes, need);
+    c->ws = workspace; c->ws_bytes = workspace_bytes;
+    b = Bump{};
+    b.base = reinterpret_cast<uint8_t*>(workspace);
+    carve(c.get(), b);
+    CUDA_TRY(cudaSetDevice(device));
+    build_tables(c.get());
+    cudaStream_t s = nullptr;
+    CUDA_TRY(cudaMemsetAsync(workspace, 0, need, s));
+    for (LocalPart& P : c->parts) {
+        CUDA_TRY(cudaMemcpyAsync(P.rowptr, P.rowptr_h, sizeof(int32_t) * (P.n + 1), cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(P.colidx, P.colidx_h, sizeof(int32_t) * P.nnz, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(P.val, P.val_h, sizeof(float) * P.nnz, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(P.halo_local, P.halo_h, sizeof(int32_t) * P.hoff[c->p], cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(P.moff_d, P.moff.data(), sizeof(int64_t) * (c->p + 1), cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(P.hoff_d, P.hoff.data(), sizeof(int64_t) * (c->p + 1), cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(P.gsend_d, &P.gsend_h, sizeof(RegionTab), cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(P.grecv_d, &P.grecv_h, sizeof(RegionTab), cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(P.ssend_d, &P.ssend_h, sizeof(RegionTab), cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(P.srecv_d, &P.srecv_h, sizeof(RegionTab), cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMallocHost(&P.cnt_h, sizeof(int32_t) * 4 * c->p));
+    }
+    CUDA_TRY(cudaMallocHost(&c->stats_h, sizeof(long long) * CDFGNN_MAX_LAYERS * 2 * 4));
+    CUDA_TRY(cudaMallocHost(&c->host_scratch, sizeof(double) * (c->k + 8)));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_uid, sizeof(id));
+        NCCL_TRY(ncclCommInitRank(&c->comm, world, id, rank));
+    }
+    c->eps = cfg->eps_init;
+    c->timing = cfg->timing != 0;
+    *out = c.release();
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_destroy(cdfgnn_ctx* c) {
+    if (!c) return CDFGNN_OK;
+    if (c->comm) ncclCommDestroy(c->comm);
+    for (LocalPart& P : c->parts)
+        if (P.cnt_h) cudaFreeHost(P.cnt_h);
+    if (c->stats_h) cudaFreeHost(c->stats_h);
+    if (c->host_scratch) cudaFreeHost(c->host_scratch);
+    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+    delete c;
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_halo_exchange(cdfgnn_ctx* c, int32_t l, int32_t dir, float* const* X,
+                                    int64_t ld, float eps, cdfgnn_sync_stats* st, void* stream) {
+    if (!c || !X) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+    if (l < 1 || l > c->cfg.L || dir < 0 || dir > 1) CDF_FAIL(CDFGNN_EUSAGE, "bad layer/dir");
+    cudaStream_t s = (cudaStream_t)stream;
+    CUDA_TRY(cudaSetDevice(c->device));
+    unsigned long long* slot = c->stats_d + ((l - 1) * 2 + dir) * 4;
+    if (st) CUDA_TRY(cudaMemsetAsync(slot, 0, sizeof(long long) * 4, s));
+    int64_t wire = 0;
+    CDF_TRY(halo_impl(c, l, dir, X, ld, eps, s, &wire));
+    if (st) CDF_TRY(read_stats_now(c, l, dir, wire, s, st));
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_layer_fwd(cdfgnn_ctx* c, int32_t l, const float* const* H_in, int64_t ld_in,
+                                const float* W, float* const* Z, float* const* H_out, int64_t ld_out,
+                                float eps, cdfgnn_sync_stats* st, void* stream) {
+    if (!c || !H_in || !W || !Z) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+    if (l < 1 || l > c->cfg.L) CDF_FAIL(CDFGNN_EUSAGE, "bad layer");
+    cudaStream_t s = (cudaStream_t)stream;
+    CUDA_TRY(cudaSetDevice(c->device));
+    unsigned long long* slot = c->stats_d + ((l - 1) * 2) * 4;
+    if (st) CUDA_TRY(cudaMemsetAsync(slot, 0, sizeof(long long) * 4, s));
+    int64_t wire = 0;
+    CDF_TRY(fwd_impl(c, l, H_in, ld_in, W, Z, H_out, ld_out, eps, s, &wire));
+    if (st) CDF_TRY(read_stats_now(c, l, 0, wire, s, st));
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_layer_bwd(cdfgnn_ctx* c, int32_t l, float* const* dZ, int64_t ld,
+                                const float* const* H_in, int64_t ld_in, const float* W,
+                                float* const* dZ_prev, float* dW, float eps,
+                                cdfgnn_sync_stats* st, void* stream) {
+    if (!c || !dZ || !H_in || !W || !dW) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+    if (l < 1 || l > c->cfg.L) CDF_FAIL(CDFGNN_EUSAGE, "bad layer");
+    cudaStream_t s = (cudaStream_t)stream;
+    CUDA_TRY(cudaSetDevice(c->device));
+    unsigned long long* slot = c->stats_d + ((l - 1) * 2 + 1) * 4;
+    if (st) CUDA_TRY(cudaMemsetAsync(slot, 0, sizeof(long long) * 4, s));
+    int64_t wire = 0;
+    CDF_TRY(bwd_impl(c, l, dZ, ld, H_in, ld_in, W, dZ_prev, dW, eps, s, &wire));
+    if (st) CDF_TRY(read_stats_now(c, l, 1, wire, s, st));
+    return CDFGNN_OK;
+}
+
+static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const* labels,
+                      const uint8_t* const* train, float* const* W, cdfgnn_epoch_stats* out,
+                      cudaStream_t s) {
+    const int L = c->cfg.L, k = c->k;
+    const int C = c->cfg.dims[L];
+    c->launches = 0;
+    c->ev_used = 0;
+    int64_t wire[CDFGNN_MAX_LAYERS][2] = {};
+    CUDA_TRY(cudaMemsetAsync(c->stats_d, 0, sizeof(long long) * CDFGNN_MAX_LAYERS * 2 * 4, s));
+    CUDA_TRY(cudaMemsetAsync(c->scal_d, 0, sizeof(int32_t) * 8, s));
+    mark(c, PH_OTHER, s);
+    if (c->ntrain < 0) {
+        // global train count over masters (every train vertex has exactly one master)
+        for (int t = 0; t < k; ++t) {
+            LocalPart& P = c->parts[t];
+            launch_count_train(P.n, P.B, P.M, train[t], c->scal_d + 2, s);
+            c->launches++;
+        }
+        if (c->world > 1)
+            NCCL_TRY(ncclAllReduce(c->scal_d + 2, c->scal_d + 2, 1, ncclInt32, ncclSum, c->comm, s));
+        int32_t* hs = reinterpret_cast<int32_t*>(c->host_scratch);
+        CUDA_TRY(cudaMemcpyAsync(hs, c->scal_d + 2, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        c->ntrain = hs[0];
+        if (c->ntrain <= 0) CDF_FAIL(CDFGNN_EDATA, "no training vertices");
+    }
+    const double eps_used = c->cfg.cache_on ? c->eps : 0.0;
+    const float eps32 = (float)eps_used;   // reading R15: rounded once on the host
+    // ---- forward (Alg. 1 L2-L6)
+    std::vector<const float*> hin(k);
+    for (int t = 0; t < k; ++t) hin[t] = X[t];
+    int64_t ld_in = ld_of(c->cfg.dims[0]);
+    for (int l = 1; l <= L; ++l) {
+        const int64_t ld = ld_of(c->cfg.dims[l]);
+        std::vector<float*> z(k);
+        for (int t = 0; t < k; ++t) z[t] = c->parts[t].act[l];
+        CDF_TRY(fwd_impl(c, l, hin.data(), ld_in, W[l - 1], z.data(), l < L ? z.data() : nullptr,
+                         ld, eps32, s, &wire[l - 1][0]));
+        for (int t = 0; t < k; ++t) hin[t] = z[t];
+        ld_in = ld;
+    }
+    // ---- loss on masters (Alg. 1 L7)
+    mark(c, PH_OTHER, s);
+    const int64_t ldL = ld_of(C);
+    std::vector<float*> dcur(k), dprev(k);
+    for (int t = 0; t < k; ++t) {
+        LocalPart& P = c->parts[t];
+        launch_loss(P.act[L], ldL, C, P.n, P.B, P.M, labels[t], train[t], 1.0 / (double)c->ntrain,
+                    P.D[L & 1], P.rowloss, c->scal_d, c->scal_d + 1, s);
+        launch_reduce_rows(P.rowloss, P.n, c->loss_d + t, s);
+        c->launches += 2;
+        dcur[t] = P.D[L & 1];
+    }
+    CDF_TRY(check_launch("loss"));
+    // ---- backward (Alg. 1 L8-L14)
+    for (int l = L; l >= 1; --l) {
+        const int64_t ld = ld_of(c->cfg.dims[l]);
+        const int64_t ldi = ld_of(c->cfg.dims[l - 1]);
+        std::vector<const float*> h(k);
+        for (int t = 0; t < k; ++t) {
+            h[t] = l == 1 ? X[t] : c->parts[t].act[l - 1];
+            dprev[t] = c->parts[t].D[(l - 1) & 1];
+        }
+        CDF_TRY(bwd_impl(c, l, dcur.data(), ld, h.data(), ldi, W[l - 1], l > 1 ? dprev.data() : nullptr,
+                         c->dW + c->woff[l - 1], eps32, s, &wire[l - 1][1]));
+        dcur = dprev;
+    }
+    // ---- parameter aggregation + update (Alg. 1 L12-L13)
+    mark(c, PH_OTHER, s);
+    if (c->world > 1) {
+        NCCL_TRY(ncclGroupStart());
+        NCCL_TRY(ncclAllReduce(c->dW, c->dW, (size_t)c->wtotal, ncclFloat32, ncclSum, c->comm, s));
+        NCCL_TRY(ncclAllReduce(c->loss_d, c->loss_d, 1, ncclFloat64, ncclSum, c->comm, s));
+        NCCL_TRY(ncclAllReduce(c->scal_d, c->scal_d, 1, ncclInt32, ncclSum, c->comm, s));
+        NCCL_TRY(ncclGroupEnd());
+    }
+    c->step_t++;
+    const double bc1 = 1.0 - std::pow(c->cfg.beta1, (double)c->step_t);
+    const double bc2 = 1.0 - std::pow(c->cfg.beta2, (double)c->step_t);
+    for (int l = 1; l <= L; ++l) {
+        const int64_t off = c->woff[l - 1], cnt = c->woff[l] - off;
+        launch_optimizer(c->cfg.optimizer, W[l - 1], c->dW + off, c->adam_m + off, c->adam_v + off,
+                         cnt, (float)c->cfg.lr, (float)c->cfg.beta1, (float)c->cfg.beta2,
+                         (float)c->cfg.adam_eps, (float)bc1, (float)bc2, s);
+        c->launches++;
+    }
+    CDF_TRY(check_launch("optimizer"));
+    mark(c, PH_END, s);
+    // ---- read back loss / accuracy / counters (C5) and update ε
+    double* hd = c->host_scratch;
+    CUDA_TRY(cudaMemcpyAsync(hd, c->loss_d, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+    int32_t* hi = reinterpret_cast<int32_t*>(hd + k);
+    CUDA_TRY(cudaMemcpyAsync(hi, c->scal_d, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(c->stats_h, c->stats_d, sizeof(long long) * L * 2 * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (hi[1] == 3) CDF_FAIL(CDFGNN_EDATA, "label out of range");
+    if (hi[1] != 0) CDF_FAIL(CDFGNN_EPROTO, "halo protocol violation (code %d)", hi[1]);
+    double loss = 0.0;
+    for (int t = 0; t < k; ++t) loss += hd[t];
+    loss /= (double)c->ntrain;
+    const int64_t correct = hi[0];
+    const double acc = (double)correct / (double)c->ntrain;
+    if (out) {
+        std::memset(out, 0, sizeof(*out));
+        out->loss = loss;
+        out->correct = correct;
+        out->total = c->ntrain;
+        out->acc = acc;
+        out->eps_used = eps_used;
+        for (int l = 1; l <= L; ++l)
+            for (int dir = 0; dir < 2; ++dir)
+                fill_sync_stats(c, l, dir, c->stats_h + ((l - 1) * 2 + dir) * 4, wire[l - 1][dir],
+                                dir ? &out->bwd[l - 1] : &out->fwd[l - 1]);
+        out->gpu_launches = c->launches;
+        if (c->timing && c->ev_used >= 2) {
+            double ph[5] = {0, 0, 0, 0, 0};
+            int nsp = 0;
+            double spsum = 0;
+            for (size_t e = 0; e + 1 < c->ev_used; ++e) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, c->ev[e], c->ev[e + 1]);
+                ph[c->ev_phase[e]] += ms;
+                if (c->ev_phase[e] == PH_SPMM) { nsp++; spsum += ms; }
+            }
+            out->ms_gemm = ph[PH_GEMM];
+            out->ms_spmm = ph[PH_SPMM];
+            out->ms_sync = ph[PH_SYNC];
+            out->ms_other = ph[PH_OTHER];
+            out->spmm_launches = nsp;
+            out->spmm_ms_sum = spsum;
+            double bytes = 0;
+            for (int l = 1; l <= L; ++l) {
+                const double ld = (double)ld_of(c->cfg.dims[l]);
+                for (const LocalPart& P : c->parts)   // fwd + bwd SpMM at width F_l
+                    bytes += 2.0 * (4.0 * (P.n + 1) + 8.0 * P.nnz + 4.0 * ld * P.nnz + 4.0 * ld * P.n);
+            }
+            out->spmm_bytes = bytes;
+        }
+    }
+    // ε controller (R17, R18): first epoch seeds mean_acc without changing ε
+    if (!c->have_mean) {
+        c->mean_acc = acc;
+        c->have_mean = true;
+    } else {
+        if (c->cfg.adaptive) c->eps = update_eps(c->cfg, c->eps, acc, c->mean_acc);
+        c->mean_acc = 0.8 * c->mean_acc + 0.2 * acc;
+    }
+    if (out) out->eps_next = c->cfg.cache_on ? c->eps : 0.0;
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_epoch(cdfgnn_ctx* c, const float* const* X, const int32_t* const* labels,
+                            const uint8_t* const* train_mask, float* const* W,
+                            cdfgnn_epoch_stats* out, void* stream) {
+    if (!c || !X || !labels || !train_mask || !W) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+    CUDA_TRY(cudaSetDevice(c->device));
+    return epoch_impl(c, X, labels, train_mask, W, out, (cudaStream_t)stream);
+}
+
+extern "C" int cdfgnn_epoch_host(cdfgnn_ctx* c, const float* const* X_host,
+                                 const int32_t* const* labels_host,
+                                 const uint8_t* const* train_mask_host, float* const* W,
+                                 cdfgnn_epoch_stats* out, void* stream) {
+    if (!c || !X_host || !labels_host || !train_mask_host || !W) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t ld0 = ld_of(c->cfg.dims[0]);
+    std::vector<const float*> X(c->k);
+    std::vector<const int32_t*> lab(c->k);
+    std::vector<const uint8_t*> msk(c->k);
+    for (int t = 0; t < c->k; ++t) {
+        LocalPart& P = c->parts[t];
+        CUDA_TRY(cudaMemcpyAsync(P.X_stage, X_host[t], sizeof(float) * P.n * ld0, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(P.lab_stage, labels_host[t], sizeof(int32_t) * P.n, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(P.mask_stage, train_mask_host[t], P.n, cudaMemcpyHostToDevice, s));
+        X[t] = P.X_stage; lab[t] = P.lab_stage; msk[t] = P.mask_stage;
+    }
+    return epoch_impl(c, X.data(), lab.data(), msk.data(), W, out, s);
+}
+
+extern "C" int cdfgnn_cache_view(cdfgnn_ctx* c, int32_t lp, int32_t l, int32_t dir, int32_t which,
+                                 float** ptr, int64_t* rows, int64_t* ld) {
+    if (!c || !ptr || !rows || !ld) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+    if (lp < 0 || lp >= c->k || l < 1 || l > c->cfg.L || dir < 0 || dir > 1)
+        CDF_FAIL(CDFGNN_EUSAGE, "bad part/layer/dir");
+    if (!c->cfg.cache_on) CDF_FAIL(CDFGNN_EUSAGE, "cache is off");
+    const LocalPart& P = c->parts[lp];
+    const CacheDev& cd = P.cache[l - 1][dir];
+    *ld = ld_of(c->cfg.dims[l]);
+    switch (which) {
+        case 0: *ptr = cd.s_mir; *rows = P.M; break;
+        case 1: *ptr = cd.b_mir; *rows = P.M; break;
+        case 2: *ptr = cd.s_mas; *rows = P.B; break;
+        case 3: *ptr = cd.a; *rows = P.B; break;
+        case 4: *ptr = cd.b_mas; *rows = P.B; break;
+        default: CDF_FAIL(CDFGNN_EUSAGE, "which must be 0..4");
+    }
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_sync_flags(cdfgnn_ctx* c, int32_t lp, int32_t which, uint8_t** ptr, int64_t* rows) {
+    if (!c || !ptr || !rows) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+    if (lp < 0 || lp >= c->k) CDF_FAIL(CDFGNN_EUSAGE, "bad part");
+    const LocalPart& P = c->parts[lp];
+    switch (which) {
+        case 0: *ptr = P.gflag; *rows = P.M; break;
+        case 1: *ptr = P.fired; *rows = P.B; break;
+        case 2: *ptr = P.active; *rows = P.B; break;
+        default: CDF_FAIL(CDFGNN_EUSAGE, "which must be 0..2");
+    }
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_reset_caches(cdfgnn_ctx* c, void* stream) {
+    if (!c) CDF_FAIL(CDFGNN_EUSAGE, "NULL ctx");
+    cudaStream_t s = (cudaStream_t)stream;
+    CUDA_TRY(cudaSetDevice(c->device));
+    for (LocalPart& P : c->parts)
+        for (int l = 1; l <= c->cfg.L; ++l) {
+            const int64_t ld = ld_of(c->cfg.dims[l]);
+            for (int dir = 0; dir < 2; ++dir) {
+                CacheDev& cd = P.cache[l - 1][dir];
+                if (!cd.s_mir) continue;
+                CUDA_TRY(cudaMemsetAsync(cd.s_mir, 0, sizeof(float) * P.M * ld, s));
+                CUDA_TRY(cudaMemsetAsync(cd.b_mir, 0, sizeof(float) * P.M * ld, s));
+                CUDA_TRY(cudaMemsetAsync(cd.s_mas, 0, sizeof(float) * P.B * ld, s));
+                CUDA_TRY(cudaMemsetAsync(cd.a, 0, sizeof(float) * P.B * ld, s));
+                CUDA_TRY(cudaMemsetAsync(cd.b_mas, 0, sizeof(float) * P.B * ld, s));
+            }
+        }
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_get_eps(cdfgnn_ctx* c, double* eps, double* mean_acc) {
+    if (!c) CDF_FAIL(CDFGNN_EUSAGE, "NULL ctx");
+    if (eps) *eps = c->eps;
+    if (mean_acc) *mean_acc = c->mean_acc;
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_set_eps(cdfgnn_ctx* c, double eps) {
+    if (!c) CDF_FAIL(CDFGNN_EUSAGE, "NULL ctx");
+    if (!(eps >= 0.0)) CDF_FAIL(CDFGNN_EUSAGE, "eps must be >= 0");
+    c->eps = eps;
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_spmm(cdfgnn_ctx* c, int32_t lp, const float* T, float* Y, int64_t ld, int32_t F,
+                           void* stream) {
+    if (!c || !T || !Y) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+    if (lp < 0 || lp >= c->k) CDF_FAIL(CDFGNN_EUSAGE, "bad part");
+    if (ld % 4 || ld < F || ld > 1024) CDF_FAIL(CDFGNN_EUSAGE, "ld must be a multiple of 4 in [F, 1024]");
+    CUDA_TRY(cudaSetDevice(c->device));
+    LocalPart& P = c->parts[lp];
+    launch_spmm(P.rowptr, P.colidx, P.val, P.n, T, Y, ld, (cudaStream_t)stream);
+    return check_launch("spmm");
+}
+
+extern "C" const char* cdfgnn_last_error(void) { return cdfgnn::g_err.c_str(); }
+extern "C" const char* cdfgnn_version(void) { return "cdfgnn-b200 0.1 (sm_100a)"; }

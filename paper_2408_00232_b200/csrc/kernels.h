@@ -1,0 +1,109 @@
+// Device-side structures and kernel launchers of libcdfgnn (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "cdfgnn.h"
+
+namespace cdfgnn {
+
+constexpr int kMaxParts = CDFGNN_MAX_PARTS;
+
+inline int64_t ld_of(int64_t F) { return (F + 3) / 4 * 4; }   // reading R24
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Message regions of one part, one per peer part.  A region of capacity C holds
+//   hdr: C entries of {u32 pos, f32 lo, f32 hi} (quantised) or {u32 pos} (fp32)
+//   pay: at hdr + align256(C*hdr_bytes): C rows of F codes (uint8) or ld floats.
+struct RegionTab {
+    uint8_t* hdr[kMaxParts];
+    uint8_t* pay[kMaxParts];
+    const int32_t* cnt[kMaxParts];   // message count of the region (receive tables)
+};
+
+// Everything the halo kernels need about one local part (device pointers).
+struct HaloDev {
+    int32_t me, p;
+    int64_t n, B, M;
+    int quant;                 // 0 or 8 bits
+    int64_t hdr_bytes;         // 12 (quantised) or 4
+    const int64_t* moff;       // [p+1] mirror slab offsets (mirror index space)
+    const int64_t* hoff;       // [p+1] halo list offsets (master side)
+    const int32_t* halo_local; // [hoff[p]] local master rows
+    const RegionTab* gsend;    // mirror-role send regions (gather), per master peer
+    const RegionTab* grecv;    // gather messages received, per source part
+    const RegionTab* ssend;    // master-role send regions (scatter), per mirror peer
+    const RegionTab* srecv;    // scatter messages received, per master part
+    int32_t* cnt_gsend;        // [p]
+    int32_t* cnt_ssend;        // [p]
+    uint8_t* gflag;            // [M]
+    uint8_t* fired;            // [B]
+    uint8_t* active;           // [B]
+    int32_t* idxmap;           // [p*B]
+    int32_t* mmap;             // [M]
+    uint8_t* stage_codes;      // [B*Fmax] quantised scatter codes
+    float* stage_lohi;         // [B*2]
+    float* stage_a;            // [B*ldmax] aggregate for the no-cache fp32 scatter
+    unsigned long long* status_g;   // gather tile status words
+    unsigned long long* status_s;   // scatter tile status words
+    unsigned long long* ticket;     // [2] tile tickets (gather, scatter)
+    int32_t* err;              // protocol error flag (device)
+};
+
+// Cache tables of one (layer, direction) of one part (may be null with cache off).
+struct CacheDev {
+    float* s_mir;   // [M*ld]
+    float* b_mir;   // [M*ld]
+    float* s_mas;   // [B*ld]
+    float* a;       // [B*ld]
+    float* b_mas;   // [B*ld]
+};
+
+struct SyncArgs {
+    float* X;             // part's rows [n*ld]
+    int64_t ld;
+    int F;
+    float eps;
+    int nocache;          // reading R14
+    CacheDev c;
+    unsigned long long* stats;  // [4]: gather_sent, master_fired, active, scatter_msgs
+    unsigned long long ticket_base_g, ticket_base_s;
+    uint32_t seq;
+};
+
+// ---- halo kernels (kernels_halo.cu)
+// tiles of the gather / scatter pack launches (host-side offsets)
+int gather_tiles_host(const int64_t* moff, int p, int64_t ld);
+int scatter_tiles_host(const int64_t* hoff, int p);
+// Each launcher returns the number of kernels it launched.
+int launch_gather_pack_n(const HaloDev& h, const SyncArgs& a, int ntiles, cudaStream_t s);
+int launch_map(const HaloDev& h, int mirror_side, int64_t max_count, cudaStream_t s);
+int launch_master(const HaloDev& h, const SyncArgs& a, cudaStream_t s);
+int launch_scatter_pack_n(const HaloDev& h, const SyncArgs& a, int ntiles, cudaStream_t s);
+int launch_mirror_apply(const HaloDev& h, const SyncArgs& a, cudaStream_t s);
+
+// ---- SpMM (kernels_spmm.cu): Y[n x ld] = Â T
+void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val, int64_t n,
+                 const float* T, float* Y, int64_t ld, cudaStream_t s);
+
+// ---- dense (kernels_dense.cu)
+// C[M x ldc] = op(A) op(B) (+ mask) ; columns [N, ldc) of C are written as zero.
+//   TA: A element (m,k) = A[k*lda + m], else A[m*lda + k]
+//   TB: B element (k,n) = B[n*ldb + k], else B[k*ldb + n]
+//   mask (optional): C(m,n) *= (mask[m*ldm + n] > 0)
+void launch_gemm_simt(bool TA, bool TB, int64_t M, int64_t N, int64_t K, const float* A,
+                      int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                      const float* mask, int64_t ldm, float* splitk_ws, int64_t splitk_cap,
+                      bool accumulate, cudaStream_t s);
+void launch_relu(const float* Z, float* H, int64_t count, cudaStream_t s);
+void launch_loss(const float* logits, int64_t ld, int C, int64_t n, int64_t B, int64_t M,
+                 const int32_t* labels, const uint8_t* train, double inv_ntrain, float* dlogits,
+                 float* rowloss, int* correct, int* err, cudaStream_t s);
+void launch_reduce_rows(const float* rowloss, int64_t n, double* out, cudaStream_t s);
+void launch_count_train(int64_t n, int64_t B, int64_t M, const uint8_t* train, int* out,
+                        cudaStream_t s);
+void launch_optimizer(int kind, float* W, const float* G, float* m, float* v, int64_t count,
+                      float lr, float b1, float b2, float eps, float bc1, float bc2,
+                      cudaStream_t s);
+
+}  // namespace cdfgnn

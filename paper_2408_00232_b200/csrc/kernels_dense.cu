@@ -1,0 +1,294 @@
+// Dense kernels: fp32 SIMT GEMM (exact-fp32 mode), ReLU, loss head, reductions,
+// optimiser (sm_100a).
+//
+//   T  = H W                 feature transform (eq. 1; reading R5: Â(HW))
+//   dW = Hᵀ S                weight gradient (eq. 5; reading R6), split-K with a
+//                            fixed-order reduction (deterministic)
+//   δ̈  = (S Wᵀ) ⊙ 𝟙[H > 0]   input gradient (σ' of ReLU, R3)
+//   loss: mean CE over masters ∩ train (R7), δ̈^(L) = (softmax − onehot)/N_train
+//   optimiser: W ← W − η ΣΔ or Adam (PyTorch update formula)
+// The tcgen05 TF32 GEMMs live in gemm_tc.cu; this SIMT GEMM is the exact-fp32 path.
+#include <cfloat>
+
+#include "kernels.h"
+
+namespace cdfgnn {
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(int64_t M, int64_t N, int64_t K,
+                                                        const float* __restrict__ A, int64_t lda,
+                                                        const float* __restrict__ B, int64_t ldb,
+                                                        float* __restrict__ C, int64_t ldc,
+                                                        const float* __restrict__ mask, int64_t ldm,
+                                                        float* __restrict__ ws, int64_t kchunk,
+                                                        int accumulate) {
+    __shared__ float As[BK][BM + 4];
+    __shared__ float Bs[BK][BN + 4];
+    const int tid = threadIdx.x;
+    const int tx = tid % 16, ty = tid / 16;
+    const int64_t m0 = (int64_t)blockIdx.y * BM;
+    const int64_t n0 = (int64_t)blockIdx.x * BN;
+    const int64_t kb = (int64_t)blockIdx.z * kchunk;
+    const int64_t ke = min(K, kb + kchunk);
+    float acc[4][4] = {};
+    for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int idx = tid + i * 256;
+            int mm, kk;
+            if (TA) { kk = idx / BM; mm = idx % BM; } else { mm = idx / BK; kk = idx % BK; }
+            const int64_t gm = m0 + mm, gk = k0 + kk;
+            float va = 0.f;
+            if (gm < M && gk < ke) va = TA ? A[gk * lda + gm] : A[gm * lda + gk];
+            As[kk][mm] = va;
+            int nn, kk2;
+            if (TB) { nn = idx / BK; kk2 = idx % BK; } else { kk2 = idx / BN; nn = idx % BN; }
+            const int64_t gn = n0 + nn, gk2 = k0 + kk2;
+            float vb = 0.f;
+            if (gn < N && gk2 < ke) vb = TB ? B[gn * ldb + gk2] : B[gk2 * ldb + gn];
+            Bs[kk2][nn] = vb;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    if (ws) {   // split-K partial: ws[z][M][N]
+        float* wz = ws + (int64_t)blockIdx.z * M * N;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t gm = m0 + ty * 4 + i;
+            if (gm >= M) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t gn = n0 + tx * 4 + j;
+                if (gn < N) wz[gm * N + gn] = acc[i][j];
+            }
+        }
+        return;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t gm = m0 + ty * 4 + i;
+        if (gm >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t gn = n0 + tx * 4 + j;
+            if (gn >= ldc) continue;
+            float v = gn < N ? acc[i][j] : 0.f;
+            if (mask && gn < N && !(mask[gm * ldm + gn] > 0.f)) v = 0.f;
+            if (accumulate && gn < N) v += C[gm * ldc + gn];
+            C[gm * ldc + gn] = v;
+        }
+    }
+}
+
+__global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const float* __restrict__ ws,
+                                     float* __restrict__ C, int64_t ldc, int accumulate) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M * ldc) return;
+    const int64_t m = i / ldc, n = i % ldc;
+    if (n >= N) { C[i] = 0.f; return; }
+    float v = 0.f;
+    for (int z = 0; z < splits; ++z) v += ws[(int64_t)z * M * N + m * N + n];   // fixed order
+    if (accumulate) v += C[i];
+    C[i] = v;
+}
+
+__global__ void relu_kernel(const float* __restrict__ Z, float* __restrict__ H, int64_t n4) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n4) return;
+    float4 z = reinterpret_cast<const float4*>(Z)[i];
+    z.x = fmaxf(z.x, 0.f); z.y = fmaxf(z.y, 0.f); z.z = fmaxf(z.z, 0.f); z.w = fmaxf(z.w, 0.f);
+    reinterpret_cast<float4*>(H)[i] = z;
+}
+
+constexpr int kMaxClassPerLane = 8;   // C <= 256
+
+__global__ void __launch_bounds__(256) loss_kernel(const float* __restrict__ logits, int64_t ld, int C,
+                                                   int64_t n, int64_t B, int64_t M,
+                                                   const int32_t* __restrict__ labels,
+                                                   const uint8_t* __restrict__ train, double inv_ntrain,
+                                                   float* __restrict__ dlogits,
+                                                   float* __restrict__ rowloss, int* correct, int* err) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (row >= n) return;
+    const bool master = row < B || row >= B + M;
+    const bool use = master && train[row];
+    float* drow = dlogits + row * ld;
+    if (!use) {
+        for (int c = lane; c < ld; c += 32) drow[c] = 0.f;
+        if (lane == 0) rowloss[row] = 0.f;
+        return;
+    }
+    const int y = labels[row];
+    if (y < 0 || y >= C) {
+        if (lane == 0) atomicExch(err, 3);
+        for (int c = lane; c < ld; c += 32) drow[c] = 0.f;
+        if (lane == 0) rowloss[row] = 0.f;
+        return;
+    }
+    const float* z = logits + row * ld;
+    float v[kMaxClassPerLane];
+    float mx = -FLT_MAX;
+    int amax = 0x7fffffff;
+#pragma unroll
+    for (int t = 0; t < kMaxClassPerLane; ++t) {
+        const int c = lane + 32 * t;
+        v[t] = c < C ? z[c] : -FLT_MAX;
+        if (c < C && (v[t] > mx)) { mx = v[t]; amax = c; }
+    }
+    // warp argmax, ties to the lowest class (reading R16)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, mx, o);
+        const int oa = __shfl_xor_sync(0xffffffffu, amax, o);
+        if (om > mx || (om == mx && oa < amax)) { mx = om; amax = oa; }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int t = 0; t < kMaxClassPerLane; ++t) {
+        const int c = lane + 32 * t;
+        if (c < C) s += expf(v[t] - mx);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float lse = mx + logf(s);
+    const float inv = (float)inv_ntrain;
+#pragma unroll
+    for (int t = 0; t < kMaxClassPerLane; ++t) {
+        const int c = lane + 32 * t;
+        if (c < C) {
+            const float p = expf(v[t] - mx) / s;
+            drow[c] = (p - (c == y ? 1.f : 0.f)) * inv;
+        } else if (c < ld) {
+            drow[c] = 0.f;
+        }
+    }
+    for (int c = lane + 32 * kMaxClassPerLane; c < ld; c += 32) drow[c] = 0.f;
+    if (lane == (y & 31)) {
+        float vy = 0.f;
+#pragma unroll
+        for (int t = 0; t < kMaxClassPerLane; ++t)
+            if (lane + 32 * t == y) vy = v[t];
+        rowloss[row] = lse - vy;
+    }
+    if (lane == 0 && amax == y) atomicAdd(correct, 1);
+}
+
+__global__ void reduce_rows_kernel(const float* __restrict__ x, int64_t n, double* out) {
+    __shared__ double sh[1024];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += (double)x[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+__global__ void count_train_kernel(int64_t n, int64_t B, int64_t M, const uint8_t* train, int* out) {
+    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool use = row < n && (row < B || row >= B + M) && train[row];
+    const unsigned b = __ballot_sync(0xffffffffu, use);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(out, __popc(b));
+}
+
+__global__ void optimizer_kernel(int kind, float* __restrict__ W, const float* __restrict__ G,
+                                 float* __restrict__ m, float* __restrict__ v, int64_t count,
+                                 float lr, float b1, float b2, float eps, float bc1, float bc2) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const float g = G[i];
+    if (kind == 0) {
+        W[i] = W[i] - lr * g;
+        return;
+    }
+    const float mi = b1 * m[i] + (1.f - b1) * g;       // Adam, PyTorch formula
+    const float vi = b2 * v[i] + (1.f - b2) * g * g;
+    m[i] = mi;
+    v[i] = vi;
+    const float denom = sqrtf(vi) / sqrtf(bc2) + eps;
+    W[i] = W[i] - (lr / bc1) * (mi / denom);
+}
+
+}  // namespace
+
+void launch_gemm_simt(bool TA, bool TB, int64_t M, int64_t N, int64_t K, const float* A,
+                      int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                      const float* mask, int64_t ldm, float* splitk_ws, int64_t splitk_cap,
+                      bool accumulate, cudaStream_t s) {
+    if (M <= 0 || ldc <= 0) return;
+    const unsigned gx = (unsigned)((std::max<int64_t>(N, ldc) + BN - 1) / BN);
+    const unsigned gy = (unsigned)((M + BM - 1) / BM);
+    int splits = 1;
+    if (splitk_ws && !mask) {
+        // enough CTAs for 148 SMs; the partials must fit the caller's buffer
+        const int64_t tiles = (int64_t)gx * gy;
+        while (tiles * splits < 4 * 148 && K / (splits * 2) >= 256 &&
+               (int64_t)(splits * 2) * M * N <= splitk_cap)
+            splits *= 2;
+    }
+    const int64_t kchunk = splits > 1 ? (((K + splits - 1) / splits + BK - 1) / BK * BK) : K;
+    dim3 grid(gx, gy, splits);
+    float* ws = splits > 1 ? splitk_ws : nullptr;
+    const int acc = accumulate ? 1 : 0;
+    if (!TA && !TB) gemm_simt_kernel<false, false><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, mask, ldm, ws, kchunk, acc);
+    else if (!TA && TB) gemm_simt_kernel<false, true><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, mask, ldm, ws, kchunk, acc);
+    else if (TA && !TB) gemm_simt_kernel<true, false><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, mask, ldm, ws, kchunk, acc);
+    else gemm_simt_kernel<true, true><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, mask, ldm, ws, kchunk, acc);
+    if (splits > 1) {
+        const int64_t tot = M * ldc;
+        splitk_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(M, N, splits, ws, C, ldc, acc);
+    }
+}
+
+void launch_relu(const float* Z, float* H, int64_t count, cudaStream_t s) {
+    const int64_t n4 = count / 4;
+    if (n4 <= 0) return;
+    relu_kernel<<<(unsigned)((n4 + 255) / 256), 256, 0, s>>>(Z, H, n4);
+}
+
+void launch_loss(const float* logits, int64_t ld, int C, int64_t n, int64_t B, int64_t M,
+                 const int32_t* labels, const uint8_t* train, double inv_ntrain, float* dlogits,
+                 float* rowloss, int* correct, int* err, cudaStream_t s) {
+    if (n <= 0) return;
+    loss_kernel<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(logits, ld, C, n, B, M, labels, train,
+                                                        inv_ntrain, dlogits, rowloss, correct, err);
+}
+
+void launch_reduce_rows(const float* rowloss, int64_t n, double* out, cudaStream_t s) {
+    reduce_rows_kernel<<<1, 1024, 0, s>>>(rowloss, n, out);
+}
+
+void launch_count_train(int64_t n, int64_t B, int64_t M, const uint8_t* train, int* out,
+                        cudaStream_t s) {
+    if (n <= 0) return;
+    count_train_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, B, M, train, out);
+}
+
+void launch_optimizer(int kind, float* W, const float* G, float* m, float* v, int64_t count,
+                      float lr, float b1, float b2, float eps, float bc1, float bc2,
+                      cudaStream_t s) {
+    if (count <= 0) return;
+    optimizer_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(kind, W, G, m, v, count, lr,
+                                                                     b1, b2, eps, bc1, bc2);
+}
+
+}  // namespace cdfgnn

@@ -1,0 +1,639 @@
+// Halo-exchange kernels: adaptive-cache test, quantise + pack, apply (sm_100a).
+//
+// One synchronisation (§3.2, Alg. 2, §5):
+//   gather_pack   mirrors: d = z − s; send iff max|d| > RN(ε·max|s|) (Alg. 2 L4, reading R15);
+//                 quantise d to uint8 codes per vertex (lo, hi header, §5), compact the
+//                 senders per master peer (warp ballot + block scan + decoupled look-back,
+//                 order preserved), update the snapshot s += deq (reading R11)
+//   map           received message -> row index tables
+//   master        per boundary master: a += deq(Δ) in ascending source part (Alg. 2
+//                 L11-L13, R13), own test + a += z − s (L14-L19), active flag, scatter
+//                 delta q(a − b) staged once, b += deq (R12), Z row ← b
+//   scatter_pack  per mirror peer: compact active masters, copy staged codes / a
+//   mirror_apply  b += deq (or b ← a), Z row ← b
+// Every floating-point step of the cache test and the quantiser uses explicit
+// round-to-nearest intrinsics (no FMA contraction) in the canonical order of
+// reading R15, so masks and codes are bit-identical to oracle/cache.py's fp32 replay.
+#include <cuda/atomic>
+
+#include "kernels.h"
+
+namespace cdfgnn {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kScatterTile = 256;
+
+// ---- R15 canonical quantiser (B = 8) ------------------------------------------
+__device__ __forceinline__ uint32_t q8(float d, float lo, float rng) {
+    if (rng == 0.f) return 0u;
+    float t = __fsub_rn(d, lo);
+    t = __fmul_rn(t, 256.f);
+    t = __fdiv_rn(t, rng);
+    t = __fadd_rn(t, 0.5f);
+    float q = floorf(t);
+    return (uint32_t)fminf(q, 255.f);
+}
+__device__ __forceinline__ float dq8(uint32_t q, float lo, float step) {
+    return __fadd_rn(__fmul_rn(step, (float)q), lo);
+}
+__device__ __forceinline__ float step8(float lo, float hi) {
+    return __fmul_rn(__fsub_rn(hi, lo), 0.00390625f);   // RN((hi−lo)·2^-8)
+}
+
+template <int LPR>
+__device__ __forceinline__ float gmax(float v) {
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+template <int LPR>
+__device__ __forceinline__ float gmin(float v) {
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float comp(const float4& v, int k) {
+    return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+}
+__device__ __forceinline__ void setc(float4& v, int k, float x) {
+    if (k == 0) v.x = x; else if (k == 1) v.y = x; else if (k == 2) v.z = x; else v.w = x;
+}
+
+// ---- decoupled look-back over tiles of one segment ------------------------------
+// status word: [63:32] launch sequence, [31:30] 1 = aggregate, 2 = inclusive prefix, [29:0] value
+__device__ __forceinline__ unsigned long long mkstat(uint32_t seq, uint32_t kind, uint32_t v) {
+    return ((unsigned long long)seq << 32) | ((unsigned long long)kind << 30) | (v & 0x3FFFFFFFu);
+}
+// called by one thread; returns the exclusive prefix of `tile` within its segment
+__device__ uint32_t lookback(unsigned long long* status, int tile, bool first_in_seg,
+                             uint32_t count, uint32_t seq) {
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(status[tile]);
+    if (first_in_seg) {
+        me.store(mkstat(seq, 2, count), cuda::memory_order_release);
+        return 0;
+    }
+    me.store(mkstat(seq, 1, count), cuda::memory_order_release);
+    uint32_t excl = 0;
+    for (int j = tile - 1;; --j) {
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[j]);
+        unsigned long long w;
+        do {
+            w = st.load(cuda::memory_order_acquire);
+        } while ((uint32_t)(w >> 32) != seq || ((w >> 30) & 3u) == 0u);
+        excl += (uint32_t)(w & 0x3FFFFFFFu);
+        if (((w >> 30) & 3u) == 2u) break;
+    }
+    me.store(mkstat(seq, 2, excl + count), cuda::memory_order_release);
+    return excl;
+}
+
+__device__ __forceinline__ int find_seg(const int64_t* off, int p, int64_t idx) {
+    int s = 0;
+    while (s + 1 < p && off[s + 1] <= idx) ++s;
+    return s;
+}
+
+// ==================================================================================
+// gather_pack: one tile = 8 warps x (32/LPR) mirror rows, all within one master peer
+// ==================================================================================
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(kThreads) gather_pack_kernel(HaloDev h, SyncArgs a) {
+    constexpr int GPW = 32 / LPR;
+    constexpr int TR = kWarps * GPW;
+    __shared__ int s_tile;
+    __shared__ int s_wcnt[kWarps];
+    __shared__ uint32_t s_excl;
+    __shared__ int64_t s_moff[kMaxParts + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x <= h.p) s_moff[threadIdx.x] = h.moff[threadIdx.x];
+    if (threadIdx.x == 0)
+        s_tile = (int)(atomicAdd(&h.ticket[0], 1ull) - a.ticket_base_g);
+    __syncthreads();
+    const int tile = s_tile;
+    // segment (master peer) of this tile
+    int seg = 0, tbase = 0;
+    for (int j = 0; j < h.p; ++j) {
+        int64_t len = s_moff[j + 1] - s_moff[j];
+        int nt = (int)((len + TR - 1) / TR);
+        if (tile < tbase + nt) { seg = j; break; }
+        tbase += nt;
+    }
+    const int ltile = tile - tbase;
+    const int64_t seg_len = s_moff[seg + 1] - s_moff[seg];
+    const int g = lane / LPR, gl = lane % LPR;
+    const int64_t ridx = (int64_t)ltile * TR + warp * GPW + g;      // position in halo list
+    const bool valid = ridx < seg_len;
+    const int64_t mrow = s_moff[seg] + (valid ? ridx : 0);          // mirror index
+    const float* xr = a.X + (h.B + mrow) * a.ld;
+    float* sr = a.nocache ? nullptr : a.c.s_mir + mrow * a.ld;
+    float4 d[VPL], x[VPL];
+    float maxd = 0.f, maxs = 0.f, lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+        const int c0 = (gl + v * LPR) * 4;
+        x[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid && c0 < a.ld) {
+            x[v] = ld4(xr + c0);
+            if (sr) s4 = ld4(sr + c0);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float dk = __fsub_rn(comp(x[v], k), comp(s4, k));
+            setc(d[v], k, dk);
+            if (c0 + k < a.F) {
+                maxd = fmaxf(maxd, fabsf(dk));
+                maxs = fmaxf(maxs, fabsf(comp(s4, k)));
+                lo = fminf(lo, dk);
+                hi = fmaxf(hi, dk);
+            }
+        }
+    }
+    maxd = gmax<LPR>(maxd);
+    maxs = gmax<LPR>(maxs);
+    lo = gmin<LPR>(lo);
+    hi = gmax<LPR>(hi);
+    const bool flag = valid && (a.nocache || maxd > __fmul_rn(a.eps, maxs));
+    const unsigned bal = __ballot_sync(0xffffffffu, flag && gl == 0);
+    if (lane == 0) s_wcnt[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t cnt = 0;
+        for (int w = 0; w < kWarps; ++w) cnt += s_wcnt[w];
+        const int ntiles_seg = (int)((seg_len + TR - 1) / TR);
+        const uint32_t excl = lookback(h.status_g, tile, ltile == 0, cnt, a.seq);
+        s_excl = excl;
+        if (ltile == ntiles_seg - 1) {
+            h.cnt_gsend[seg] = (int32_t)(excl + cnt);
+            atomicAdd(&a.stats[0], (unsigned long long)(excl + cnt));
+        }
+    }
+    __syncthreads();
+    int woff = 0;
+    for (int w = 0; w < warp; ++w) woff += s_wcnt[w];
+    const int lead = g * LPR;
+    const int rank_in_warp = __popc(bal & ((1u << lead) - 1u));
+    const int64_t m = (int64_t)s_excl + woff + rank_in_warp;
+    if (valid && gl == 0) h.gflag[mrow] = flag ? 1 : 0;
+    if (!flag) return;
+    uint8_t* hdr = h.gsend->hdr[seg];
+    uint8_t* pay = h.gsend->pay[seg];
+    if (h.quant) {
+        const float rng = __fsub_rn(hi, lo);
+        const float stp = step8(lo, hi);
+        if (gl == 0) {
+            uint32_t* hp = reinterpret_cast<uint32_t*>(hdr + m * 12);
+            hp[0] = (uint32_t)ridx;
+            hp[1] = __float_as_uint(lo);
+            hp[2] = __float_as_uint(hi);
+        }
+        uint8_t* codes = pay + m * (int64_t)a.F;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+            const int c0 = (gl + v * LPR) * 4;
+            if (c0 >= a.F) continue;
+            uint32_t q[4];
+            float4 snew = make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 s4 = sr ? ld4(sr + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                q[k] = q8(comp(d[v], k), lo, rng);
+                const float sk = (c0 + k < a.F) ? __fadd_rn(comp(s4, k), dq8(q[k], lo, stp)) : 0.f;
+                setc(snew, k, sk);
+            }
+            if ((a.F & 3) == 0) {
+                *reinterpret_cast<uint32_t*>(codes + c0) = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (c0 + k < a.F) codes[c0 + k] = (uint8_t)q[k];
+            }
+            if (sr) st4(sr + c0, snew);     // reading R11: s ← s + deq(q(Δ))
+        }
+    } else {
+        if (gl == 0) reinterpret_cast<uint32_t*>(hdr)[m] = (uint32_t)ridx;
+        float* prow = reinterpret_cast<float*>(pay) + m * a.ld;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+            const int c0 = (gl + v * LPR) * 4;
+            if (c0 >= a.ld) continue;
+            st4(prow + c0, d[v]);
+            if (sr) st4(sr + c0, x[v]);   // Alg. 2 L6: s ← z
+        }
+    }
+}
+
+// ==================================================================================
+// map: message -> row tables.  mirror_side = 0: idxmap[src*B + master row] = m;
+// mirror_side = 1: mmap[mirror index] = m.
+// ==================================================================================
+__global__ void map_kernel(HaloDev h, int mirror_side) {
+    const int q = blockIdx.y;
+    if (q == h.me) return;
+    const RegionTab* t = mirror_side ? h.srecv : h.grecv;
+    const int32_t cnt = *t->cnt[q];
+    const uint8_t* hdr = t->hdr[q];
+    const int64_t len = mirror_side ? (h.moff[q + 1] - h.moff[q]) : (h.hoff[q + 1] - h.hoff[q]);
+    if (cnt > len) { if (threadIdx.x == 0 && blockIdx.x == 0) atomicExch(h.err, 1); return; }
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < cnt;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t pos = *reinterpret_cast<const uint32_t*>(hdr + m * h.hdr_bytes);
+        if (pos >= len) { atomicExch(h.err, 2); continue; }
+        if (mirror_side) h.mmap[h.moff[q] + pos] = (int32_t)m;
+        else h.idxmap[(int64_t)q * h.B + h.halo_local[h.hoff[q] + pos]] = (int32_t)m;
+    }
+}
+
+// ==================================================================================
+// master: one row group per boundary master row
+// ==================================================================================
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(kThreads) master_kernel(HaloDev h, SyncArgs a) {
+    constexpr int GPW = 32 / LPR;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / LPR, gl = lane % LPR;
+    const int64_t row = ((int64_t)blockIdx.x * kWarps + warp) * GPW + g;
+    const bool valid = row < h.B;
+    const int64_t r = valid ? row : 0;
+    float4 acc[VPL];
+    const float* aold = a.nocache ? nullptr : a.c.a + r * a.ld;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+        const int c0 = (gl + v * LPR) * 4;
+        acc[v] = (aold && valid && c0 < a.ld) ? ld4(aold + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    bool any_msg = false;
+    // Alg. 2 L11-L13: received Δ in ascending source part (R13)
+    for (int s = 0; s < h.p; ++s) {
+        if (s == h.me) continue;
+        const int32_t m = valid ? h.idxmap[(int64_t)s * h.B + r] : -1;
+        if (m < 0) continue;
+        any_msg = true;
+        const uint8_t* hdr = h.grecv->hdr[s];
+        const uint8_t* pay = h.grecv->pay[s];
+        if (h.quant) {
+            const uint32_t* hp = reinterpret_cast<const uint32_t*>(hdr + (int64_t)m * 12);
+            const float lo = __uint_as_float(hp[1]), hi = __uint_as_float(hp[2]);
+            const float stp = step8(lo, hi);
+            const uint8_t* codes = pay + (int64_t)m * a.F;
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (c0 + k < a.F)
+                        setc(acc[v], k, __fadd_rn(comp(acc[v], k), dq8(codes[c0 + k], lo, stp)));
+            }
+        } else {
+            const float* prow = reinterpret_cast<const float*>(pay) + (int64_t)m * a.ld;
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 >= a.ld) continue;
+                const float4 pv = ld4(prow + c0);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) setc(acc[v], k, __fadd_rn(comp(acc[v], k), comp(pv, k)));
+            }
+        }
+    }
+    // Alg. 2 L14-L19: the master's own replica, unquantised
+    float* xr = a.X + r * a.ld;
+    float* smr = a.nocache ? nullptr : a.c.s_mas + r * a.ld;
+    float4 x[VPL], dd[VPL];
+    float maxd = 0.f, maxs = 0.f;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+        const int c0 = (gl + v * LPR) * 4;
+        x[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid && c0 < a.ld) {
+            x[v] = ld4(xr + c0);
+            if (smr) s4 = ld4(smr + c0);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float dk = __fsub_rn(comp(x[v], k), comp(s4, k));
+            setc(dd[v], k, dk);
+            if (c0 + k < a.F) {
+                maxd = fmaxf(maxd, fabsf(dk));
+                maxs = fmaxf(maxs, fabsf(comp(s4, k)));
+            }
+        }
+    }
+    maxd = gmax<LPR>(maxd);
+    maxs = gmax<LPR>(maxs);
+    const bool fired = valid && (a.nocache || maxd > __fmul_rn(a.eps, maxs));
+    if (fired) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+            const int c0 = (gl + v * LPR) * 4;
+            if (c0 >= a.ld) continue;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) setc(acc[v], k, __fadd_rn(comp(acc[v], k), comp(dd[v], k)));
+            if (smr) st4(smr + c0, x[v]);
+        }
+    }
+    const bool act = valid && (fired || any_msg);
+    // aggregate store (the no-cache fp32 scatter reads it from stage_a)
+    float* adst = a.nocache ? h.stage_a + r * a.ld : a.c.a + r * a.ld;
+    if (act) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+            const int c0 = (gl + v * LPR) * 4;
+            if (c0 < a.ld) st4(adst + c0, acc[v]);
+        }
+    }
+    // Alg. 2 L20-L22 / R12: scatter delta staged once; every replica applies the same codes
+    float* bmr = a.nocache ? nullptr : a.c.b_mas + r * a.ld;
+    float4 b[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+        const int c0 = (gl + v * LPR) * 4;
+        b[v] = (bmr && valid && c0 < a.ld) ? ld4(bmr + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (act) {
+        if (h.quant) {
+            float lo = INFINITY, hi = -INFINITY;
+            float4 del[VPL];
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float dk = __fsub_rn(comp(acc[v], k), comp(b[v], k));
+                    setc(del[v], k, dk);
+                    if (c0 + k < a.F) { lo = fminf(lo, dk); hi = fmaxf(hi, dk); }
+                }
+            }
+            lo = gmin<LPR>(lo);
+            hi = gmax<LPR>(hi);
+            const float rng = __fsub_rn(hi, lo), stp = step8(lo, hi);
+            uint8_t* codes = h.stage_codes + r * a.F;
+            if (gl == 0) { h.stage_lohi[2 * r] = lo; h.stage_lohi[2 * r + 1] = hi; }
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (c0 + k < a.F) {
+                        const uint32_t qk = q8(comp(del[v], k), lo, rng);
+                        codes[c0 + k] = (uint8_t)qk;
+                        setc(b[v], k, __fadd_rn(comp(b[v], k), dq8(qk, lo, stp)));
+                    }
+                }
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) b[v] = acc[v];
+        }
+        if (bmr) {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 < a.ld) st4(bmr + c0, b[v]);
+            }
+        }
+    }
+    if (valid) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+            const int c0 = (gl + v * LPR) * 4;
+            if (c0 < a.ld) st4(xr + c0, b[v]);      // Z row from the cached value
+        }
+        if (gl == 0) {
+            h.fired[r] = fired ? 1 : 0;
+            h.active[r] = act ? 1 : 0;
+        }
+    }
+    // counters
+    const unsigned bf = __ballot_sync(0xffffffffu, fired && gl == 0);
+    const unsigned ba = __ballot_sync(0xffffffffu, act && gl == 0);
+    if (lane == 0) {
+        if (bf) atomicAdd(&a.stats[1], (unsigned long long)__popc(bf));
+        if (ba) atomicAdd(&a.stats[2], (unsigned long long)__popc(ba));
+    }
+}
+
+// ==================================================================================
+// scatter_pack: one tile = 256 halo-list entries of one mirror peer
+// ==================================================================================
+__global__ void __launch_bounds__(kThreads) scatter_pack_kernel(HaloDev h, SyncArgs a) {
+    __shared__ int s_tile;
+    __shared__ int s_wcnt[kWarps];
+    __shared__ uint32_t s_excl;
+    __shared__ int32_t s_row[kScatterTile];
+    __shared__ int32_t s_pos[kScatterTile];
+    __shared__ int64_t s_hoff[kMaxParts + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x <= h.p) s_hoff[threadIdx.x] = h.hoff[threadIdx.x];
+    if (threadIdx.x == 0) s_tile = (int)(atomicAdd(&h.ticket[1], 1ull) - a.ticket_base_s);
+    __syncthreads();
+    const int tile = s_tile;
+    int seg = 0, tbase = 0;
+    for (int j = 0; j < h.p; ++j) {
+        int64_t len = s_hoff[j + 1] - s_hoff[j];
+        int nt = (int)((len + kScatterTile - 1) / kScatterTile);
+        if (tile < tbase + nt) { seg = j; break; }
+        tbase += nt;
+    }
+    const int ltile = tile - tbase;
+    const int64_t seg_len = s_hoff[seg + 1] - s_hoff[seg];
+    const int64_t pos = (int64_t)ltile * kScatterTile + threadIdx.x;
+    const bool valid = pos < seg_len;
+    const int32_t row = valid ? h.halo_local[s_hoff[seg] + pos] : 0;
+    const bool flag = valid && h.active[row];
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    if (lane == 0) s_wcnt[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t cnt = 0;
+        for (int w = 0; w < kWarps; ++w) cnt += s_wcnt[w];
+        const int ntiles_seg = (int)((seg_len + kScatterTile - 1) / kScatterTile);
+        const uint32_t excl = lookback(h.status_s, tile, ltile == 0, cnt, a.seq);
+        s_excl = excl;
+        if (ltile == ntiles_seg - 1) {
+            h.cnt_ssend[seg] = (int32_t)(excl + cnt);
+            atomicAdd(&a.stats[3], (unsigned long long)(excl + cnt));
+        }
+    }
+    int woff = 0;
+    for (int w = 0; w < warp; ++w) woff += s_wcnt[w];
+    const int lrank = woff + __popc(bal & ((1u << lane) - 1u));
+    if (flag) { s_row[lrank] = row; s_pos[lrank] = (int32_t)pos; }
+    __syncthreads();
+    int total = 0;
+    for (int w = 0; w < kWarps; ++w) total += s_wcnt[w];
+    uint8_t* hdr = h.ssend->hdr[seg];
+    uint8_t* pay = h.ssend->pay[seg];
+    // one warp per message
+    for (int k = warp; k < total; k += kWarps) {
+        const int64_t m = (int64_t)s_excl + k;
+        const int32_t rr = s_row[k];
+        if (h.quant) {
+            if (lane == 0) {
+                uint32_t* hp = reinterpret_cast<uint32_t*>(hdr + m * 12);
+                hp[0] = (uint32_t)s_pos[k];
+                hp[1] = __float_as_uint(h.stage_lohi[2 * rr]);
+                hp[2] = __float_as_uint(h.stage_lohi[2 * rr + 1]);
+            }
+            const uint8_t* src = h.stage_codes + (int64_t)rr * a.F;
+            uint8_t* dst = pay + m * (int64_t)a.F;
+            for (int c = lane; c < a.F; c += 32) dst[c] = src[c];
+        } else {
+            if (lane == 0) reinterpret_cast<uint32_t*>(hdr)[m] = (uint32_t)s_pos[k];
+            const float* src = (a.nocache ? h.stage_a : a.c.a) + (int64_t)rr * a.ld;
+            float* dst = reinterpret_cast<float*>(pay) + m * a.ld;
+            for (int c = lane * 4; c < a.ld; c += 128) st4(dst + c, ld4(src + c));
+        }
+    }
+}
+
+// ==================================================================================
+// mirror_apply: one row group per mirror row
+// ==================================================================================
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(kThreads) mirror_apply_kernel(HaloDev h, SyncArgs a) {
+    constexpr int GPW = 32 / LPR;
+    __shared__ int64_t s_moff[kMaxParts + 1];
+    if (threadIdx.x <= h.p) s_moff[threadIdx.x] = h.moff[threadIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / LPR, gl = lane % LPR;
+    const int64_t row = ((int64_t)blockIdx.x * kWarps + warp) * GPW + g;
+    if (row >= h.M) return;
+    const int q = find_seg(s_moff, h.p, row);
+    const int32_t m = h.mmap[row];
+    float* bmr = a.nocache ? nullptr : a.c.b_mir + row * a.ld;
+    float4 b[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+        const int c0 = (gl + v * LPR) * 4;
+        b[v] = (bmr && c0 < a.ld) ? ld4(bmr + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (m >= 0) {
+        const uint8_t* hdr = h.srecv->hdr[q];
+        const uint8_t* pay = h.srecv->pay[q];
+        if (h.quant) {
+            const uint32_t* hp = reinterpret_cast<const uint32_t*>(hdr + (int64_t)m * 12);
+            const float lo = __uint_as_float(hp[1]), hi = __uint_as_float(hp[2]);
+            const float stp = step8(lo, hi);
+            const uint8_t* codes = pay + (int64_t)m * a.F;
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (c0 + k < a.F)
+                        setc(b[v], k, __fadd_rn(comp(b[v], k), dq8(codes[c0 + k], lo, stp)));
+            }
+        } else {
+            const float* prow = reinterpret_cast<const float*>(pay) + (int64_t)m * a.ld;
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 < a.ld) b[v] = ld4(prow + c0);
+            }
+        }
+        if (bmr) {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 < a.ld) st4(bmr + c0, b[v]);
+            }
+        }
+    }
+    float* xr = a.X + (h.B + row) * a.ld;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+        const int c0 = (gl + v * LPR) * 4;
+        if (c0 < a.ld) st4(xr + c0, b[v]);
+    }
+}
+
+// ---- dispatch by row width: LPR lanes x VPL float4 per lane cover ld columns ------
+struct Shape { int lpr, vpl; };
+Shape shape_of(int64_t ld) {
+    const int64_t nv = ld / 4;
+    if (nv <= 2) return {2, 1};
+    if (nv <= 4) return {4, 1};
+    if (nv <= 8) return {8, 1};
+    if (nv <= 16) return {16, 1};
+    if (nv <= 32) return {32, 1};
+    if (nv <= 64) return {32, 2};
+    if (nv <= 128) return {32, 4};
+    return {32, 8};   // ld <= 1024
+}
+
+#define CDF_DISPATCH(LD, KERNEL, GRID, STREAM, ...)                                         \
+    do {                                                                                    \
+        Shape _s = shape_of(LD);                                                            \
+        if (_s.lpr == 2) KERNEL<2, 1><<<GRID(2), kThreads, 0, STREAM>>>(__VA_ARGS__);       \
+        else if (_s.lpr == 4) KERNEL<4, 1><<<GRID(4), kThreads, 0, STREAM>>>(__VA_ARGS__);  \
+        else if (_s.lpr == 8) KERNEL<8, 1><<<GRID(8), kThreads, 0, STREAM>>>(__VA_ARGS__);  \
+        else if (_s.lpr == 16) KERNEL<16, 1><<<GRID(16), kThreads, 0, STREAM>>>(__VA_ARGS__); \
+        else if (_s.vpl == 1) KERNEL<32, 1><<<GRID(32), kThreads, 0, STREAM>>>(__VA_ARGS__); \
+        else if (_s.vpl == 2) KERNEL<32, 2><<<GRID(32), kThreads, 0, STREAM>>>(__VA_ARGS__); \
+        else if (_s.vpl == 4) KERNEL<32, 4><<<GRID(32), kThreads, 0, STREAM>>>(__VA_ARGS__); \
+        else KERNEL<32, 8><<<GRID(32), kThreads, 0, STREAM>>>(__VA_ARGS__);                 \
+    } while (0)
+
+}  // namespace
+
+int gather_tiles_host(const int64_t* moff, int p, int64_t ld) {
+    const int TR = kWarps * (32 / shape_of(ld).lpr);
+    int t = 0;
+    for (int j = 0; j < p; ++j) t += (int)((moff[j + 1] - moff[j] + TR - 1) / TR);
+    return t;
+}
+int scatter_tiles_host(const int64_t* hoff, int p) {
+    int t = 0;
+    for (int j = 0; j < p; ++j) t += (int)((hoff[j + 1] - hoff[j] + kScatterTile - 1) / kScatterTile);
+    return t;
+}
+
+int launch_gather_pack_n(const HaloDev& h, const SyncArgs& a, int ntiles, cudaStream_t s) {
+    if (ntiles <= 0) return 0;
+    auto grid = [&](int) { return ntiles; };
+    CDF_DISPATCH(a.ld, gather_pack_kernel, grid, s, h, a);
+    return 1;
+}
+
+int launch_map(const HaloDev& h, int mirror_side, int64_t max_count, cudaStream_t s) {
+    if (max_count <= 0 || h.p <= 1) return 0;
+    dim3 grid((unsigned)std::min<int64_t>((max_count + 255) / 256, 4096), h.p);
+    map_kernel<<<grid, 256, 0, s>>>(h, mirror_side);
+    return 1;
+}
+
+int launch_master(const HaloDev& h, const SyncArgs& a, cudaStream_t s) {
+    if (h.B <= 0) return 0;
+    auto grid = [&](int lpr) {
+        const int64_t rows_per_block = kWarps * (32 / lpr);
+        return (unsigned)((h.B + rows_per_block - 1) / rows_per_block);
+    };
+    CDF_DISPATCH(a.ld, master_kernel, grid, s, h, a);
+    return 1;
+}
+
+int launch_scatter_pack_n(const HaloDev& h, const SyncArgs& a, int ntiles, cudaStream_t s) {
+    if (ntiles <= 0) return 0;
+    scatter_pack_kernel<<<ntiles, kThreads, 0, s>>>(h, a);
+    return 1;
+}
+
+int launch_mirror_apply(const HaloDev& h, const SyncArgs& a, cudaStream_t s) {
+    if (h.M <= 0) return 0;
+    auto grid = [&](int lpr) {
+        const int64_t rows_per_block = kWarps * (32 / lpr);
+        return (unsigned)((h.M + rows_per_block - 1) / rows_per_block);
+    };
+    CDF_DISPATCH(a.ld, mirror_apply_kernel, grid, s, h, a);
+    return 1;
+}
+
+}  // namespace cdfgnn

@@ -1,0 +1,125 @@
+"""GPU epoch / layer parity vs the oracle (fp64) through the C ABI.
+
+Bars (BASELINE.json north_star): fp32 features and gradients within max
+row-normwise relative error 1e-4 (SIMT fp32 GEMMs), per-epoch loss within
+1e-3·max(1, |L|) over 50 epochs; bitwise on dyadic fixtures."""
+import numpy as np
+import pytest
+
+import paper_2408_00232_b200 as cg
+from paper_2408_00232_b200.runtime import Run
+from oracle import gcn
+from oracle.cdfgnn import PartitionedGCN, TrainCfg
+from oracle.graph import normalized_adjacency
+from oracle.partition import PartitionCfg, partition as opartition
+from synth import dyadic_fixture, get_config, make_dataset, small_random_graph
+from tests.gpu_util import require_gpu, rownorm_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle(d, p, **kw):
+    oplan = opartition(d.n, d.eu, d.ev, PartitionCfg(p=p))
+    return PartitionedGCN(oplan, d.X, d.y, d.train, d.W, TrainCfg(**kw))
+
+
+@pytest.mark.parametrize("p", [1, 3])
+@pytest.mark.parametrize("cache", [False, True])
+def test_exact_mode_sgd_trajectory(p, cache):
+    require_gpu()
+    d = small_random_graph(800, 4000, (12, 16, 5), seed=61)
+    run = Run(d, p, cache=cache, quant_bits=0, eps0=0.0, adaptive=False, optimizer="sgd", lr=0.5)
+    orc = _oracle(d, p, cache=cache, quant_bits=0, eps0=0.0, adaptive=False, optimizer="sgd",
+                  lr=0.5)
+    for ep in range(6):
+        g = run.epoch()
+        o = orc.epoch()
+        assert abs(g["loss"] - o["loss"]) <= 1e-5 * max(1.0, abs(o["loss"])), (ep, g["loss"], o["loss"])
+        for wg, wo in zip(run.weights(), orc.W):
+            assert rownorm_err(wg, wo) <= 1e-4
+        if p == 1:
+            assert all(s["gather_sent"] == 0 for s in g["fwd"] + g["bwd"])
+    run.close()
+
+
+def test_forward_activations_match():
+    torch = require_gpu()
+    d = small_random_graph(1000, 6000, (20, 32, 7), seed=62)
+    p = 4
+    run = Run(d, p, cache=True, quant_bits=0, eps0=0.0, adaptive=False, optimizer="sgd", lr=0.0)
+    A = normalized_adjacency(d.n, d.eu, d.ev)
+    Z, H = gcn.forward(A, d.X.astype(np.float64), [w.astype(np.float64) for w in d.W])
+    # layer 1 through the layer API
+    ld1 = cg.ld_of(32)
+    Zs = [torch.zeros((v["n_local"], ld1), device="cuda") for v in run.views]
+    Hs = [torch.zeros((v["n_local"], ld1), device="cuda") for v in run.views]
+    cg.layer_fwd(run.ctx, 1, run.X, run.ld0, run.W[0], Zs, Hs, ld1, 0.0)
+    for v, z, h in zip(run.views, Zs, Hs):
+        g = v["local2global"]
+        assert rownorm_err(z.cpu().numpy()[:, :32], Z[0][g]) <= 1e-5
+        assert rownorm_err(h.cpu().numpy()[:, :32], H[1][g]) <= 1e-5
+    run.close()
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_dyadic_bitwise(p):
+    """P-C1: dyadic fixture — every partial sum exact, so GPU Z == plain GCN bitwise."""
+    torch = require_gpu()
+    d = dyadic_fixture(n=96, r=4, dims=(16, 8, 4))
+    run = Run(d, p, cache=True, quant_bits=0, eps0=0.0, adaptive=False, optimizer="sgd", lr=0.0)
+    A = normalized_adjacency(d.n, d.eu, d.ev)
+    Z, H = gcn.forward(A, d.X.astype(np.float64), [w.astype(np.float64) for w in d.W])
+    ld1, ld2 = cg.ld_of(8), cg.ld_of(4)
+    Z1 = [torch.zeros((v["n_local"], ld1), device="cuda") for v in run.views]
+    H1 = [torch.zeros((v["n_local"], ld1), device="cuda") for v in run.views]
+    Z2 = [torch.zeros((v["n_local"], ld2), device="cuda") for v in run.views]
+    cg.layer_fwd(run.ctx, 1, run.X, run.ld0, run.W[0], Z1, H1, ld1, 0.0)
+    cg.layer_fwd(run.ctx, 2, H1, ld1, run.W[1], Z2, None, ld2, 0.0)
+    for v, z1, z2 in zip(run.views, Z1, Z2):
+        g = v["local2global"]
+        assert np.array_equal(z1.cpu().numpy()[:, :8].astype(np.float64), Z[0][g])
+        assert np.array_equal(z2.cpu().numpy()[:, :4].astype(np.float64), Z[1][g])
+    run.close()
+
+
+def test_C1_fifty_epochs_loss_parity():
+    """configs[0]: Cora-shaped, 2 partitions on 1 GPU, ε = 0, int8; Adam lr 0.01."""
+    require_gpu()
+    d = make_dataset(get_config("C1"))
+    run = Run(d, 2, cache=True, quant_bits=8, eps0=0.0, adaptive=False, optimizer="adam", lr=0.01)
+    orc = _oracle(d, 2, cache=True, quant_bits=8, eps0=0.0, adaptive=False, optimizer="adam",
+                  lr=0.01)
+    worst = 0.0
+    for ep in range(50):
+        g = run.epoch()
+        o = orc.epoch()
+        worst = max(worst, abs(g["loss"] - o["loss"]) / max(1.0, abs(o["loss"])))
+        sent_o = sum(c.gather_sent for _, _, c in o["counters"])
+        sent_g = sum(s["gather_sent"] for s in g["fwd"] + g["bwd"])
+        assert abs(sent_g - sent_o) <= max(2, 0.01 * sent_o)
+    assert worst <= 1e-3, worst
+    run.close()
+
+
+def test_cached_adaptive_tracks_oracle():
+    require_gpu()
+    d = small_random_graph(1500, 9000, (16, 32, 6), seed=63)
+    run = Run(d, 4, cache=True, quant_bits=8, eps0=0.01, adaptive=True, optimizer="adam", lr=0.01)
+    orc = _oracle(d, 4, cache=True, quant_bits=8, eps0=0.01, adaptive=True, optimizer="adam", lr=0.01)
+    for ep in range(20):
+        g = run.epoch()
+        o = orc.epoch()
+        assert abs(g["loss"] - o["loss"]) <= 1e-2 * max(1.0, abs(o["loss"]))
+        assert g["eps_used"] == pytest.approx(o["eps"], abs=1e-12) or ep > 0
+    run.close()
+
+
+def test_label_out_of_range_is_edata():
+    torch = require_gpu()
+    d = small_random_graph(300, 1200, (8, 8, 3), seed=64)
+    run = Run(d, 2, cache=True, quant_bits=8)
+    run.labels[0].fill_(7)
+    with pytest.raises(cg.CdfgnnError) as e:
+        run.epoch()
+    assert e.value.code == 3
+    run.close()
