@@ -52,9 +52,12 @@ class Plan:
         return self._h
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _c.cdfgnn_plan_free(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) and _c is not None:
+                _c.cdfgnn_plan_free(self._h)
+                self._h = None
+        except Exception:
+            pass
 
 
 def partition(n: int, eu: np.ndarray, ev: np.ndarray, p: int, num_hosts: int = 1,

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -316,8 +317,19 @@ void build_tables(cdfgnn_ctx* c) {
     }
 }
 
+// CDFGNN_DEBUG_SYNC=1: synchronise after every launch group to localise faults
+bool debug_sync() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("CDFGNN_DEBUG_SYNC");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 int check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && debug_sync()) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) CDF_FAIL(CDFGNN_ECUDA, "%s: %s", what, cudaGetErrorString(e));
     return CDFGNN_OK;
 }

@@ -356,22 +356,25 @@ __global__ void __launch_bounds__(kThreads) master_kernel(HaloDev h, SyncArgs a)
         const int c0 = (gl + v * LPR) * 4;
         b[v] = (bmr && valid && c0 < a.ld) ? ld4(bmr + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    // scatter delta and its range, reduced by every lane of the warp (shuffles stay converged)
+    float4 del[VPL];
+    float lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+        const int c0 = (gl + v * LPR) * 4;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float dk = __fsub_rn(comp(acc[v], k), comp(b[v], k));
+            setc(del[v], k, dk);
+            if (c0 + k < a.F) { lo = fminf(lo, dk); hi = fmaxf(hi, dk); }
+        }
+    }
+    if (h.quant) {
+        lo = gmin<LPR>(lo);
+        hi = gmax<LPR>(hi);
+    }
     if (act) {
         if (h.quant) {
-            float lo = INFINITY, hi = -INFINITY;
-            float4 del[VPL];
-#pragma unroll
-            for (int v = 0; v < VPL; ++v) {
-                const int c0 = (gl + v * LPR) * 4;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const float dk = __fsub_rn(comp(acc[v], k), comp(b[v], k));
-                    setc(del[v], k, dk);
-                    if (c0 + k < a.F) { lo = fminf(lo, dk); hi = fmaxf(hi, dk); }
-                }
-            }
-            lo = gmin<LPR>(lo);
-            hi = gmax<LPR>(hi);
             const float rng = __fsub_rn(hi, lo), stp = step8(lo, hi);
             uint8_t* codes = h.stage_codes + r * a.F;
             if (gl == 0) { h.stage_lohi[2 * r] = lo; h.stage_lohi[2 * r + 1] = hi; }
