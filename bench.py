@@ -114,42 +114,50 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle leg
-def oracle_epoch_cost(ds, frac, seed=0):
+class OracleSample:
     """Estimated ms of one oracle epoch (oracle/gcn.py, fp64, p = 1) on this host.
 
     Sample: every dense op (GEMMs, ReLU, loss) runs at full size on operands of the
     right shape; each SpMM (scipy CSR, single-threaded) runs on a random `frac` row
-    sample of Â and is scaled by 1/frac."""
-    import numpy as np
-    from oracle import gcn
-    from oracle.graph import normalized_adjacency
-    rng = np.random.default_rng(seed)
-    A = normalized_adjacency(ds.n, ds.eu, ds.ev)
-    rows = np.sort(rng.choice(ds.n, max(1, int(frac * ds.n)), replace=False))
-    As = A[rows]
-    W = [w.astype(np.float64) for w in ds.W]
-    X = ds.X.astype(np.float64)
-    L = len(W)
-    t_dense = 0.0
-    t_spmm = 0.0
-    H = [X]
-    for l in range(1, L + 1):
-        t0 = time.perf_counter(); T = H[l - 1] @ W[l - 1]; t_dense += time.perf_counter() - t0
-        t0 = time.perf_counter(); _ = As @ T; t_spmm += time.perf_counter() - t0
-        t0 = time.perf_counter(); Hn = gcn.relu(T) if l < L else T; t_dense += time.perf_counter() - t0
-        H.append(Hn)
-    t0 = time.perf_counter()
-    _, delta, _ = gcn.loss_grad(H[L], ds.y, ds.train)
-    t_dense += time.perf_counter() - t0
-    for l in range(L, 0, -1):
-        t0 = time.perf_counter(); _ = As @ delta; t_spmm += time.perf_counter() - t0
-        S = delta                                   # full-size stand-in of Â δ
+    sample of Â and is scaled by 1/frac.  Â is built once, outside the timing."""
+
+    def __init__(self, ds, frac):
+        import numpy as np
+        from oracle.graph import normalized_adjacency
+        self.ds, self.frac = ds, frac
+        self.A = normalized_adjacency(ds.n, ds.eu, ds.ev)
+        self.W = [w.astype(np.float64) for w in ds.W]
+        self.X = ds.X.astype(np.float64)
+
+    def epoch_ms(self, seed=0):
+        import numpy as np
+        from oracle import gcn
+        ds, frac, W = self.ds, self.frac, self.W
+        rng = np.random.default_rng(seed)
+        rows = np.sort(rng.choice(ds.n, max(1, int(frac * ds.n)), replace=False))
+        As = self.A[rows]
+        L = len(W)
+        t_dense = 0.0
+        t_spmm = 0.0
+        H = [self.X]
+        for l in range(1, L + 1):
+            t0 = time.perf_counter(); T = H[l - 1] @ W[l - 1]; t_dense += time.perf_counter() - t0
+            t0 = time.perf_counter(); _ = As @ T; t_spmm += time.perf_counter() - t0
+            t0 = time.perf_counter(); Hn = gcn.relu(T) if l < L else T
+            t_dense += time.perf_counter() - t0
+            H.append(Hn)
         t0 = time.perf_counter()
-        _ = H[l - 1].T @ S
-        if l > 1:
-            delta = (S @ W[l - 1].T) * (H[l - 1] > 0)
+        _, delta, _ = gcn.loss_grad(H[L], ds.y, ds.train)
         t_dense += time.perf_counter() - t0
-    return 1e3 * (t_dense + t_spmm / frac)
+        for l in range(L, 0, -1):
+            t0 = time.perf_counter(); _ = As @ delta; t_spmm += time.perf_counter() - t0
+            S = delta                                   # full-size stand-in of Â δ
+            t0 = time.perf_counter()
+            _ = H[l - 1].T @ S
+            if l > 1:
+                delta = (S @ W[l - 1].T) * (H[l - 1] > 0)
+            t_dense += time.perf_counter() - t0
+        return 1e3 * (t_dense + t_spmm / frac)
 
 
 def cpu_cores():
@@ -166,9 +174,10 @@ def reference_main(args):
     from synth import get_config
     from synth.cache import cached_dataset
     ds = cached_dataset(get_config(args.config), args.scale)
+    orc = OracleSample(ds, args.cpu_frac)
     for _ in range(args.warmup):
-        oracle_epoch_cost(ds, args.cpu_frac, seed=1)
-    vals = [oracle_epoch_cost(ds, args.cpu_frac, seed=2 + k) for k in range(args.steps)]
+        orc.epoch_ms(seed=1)
+    vals = [orc.epoch_ms(seed=2 + k) for k in range(args.steps)]
     v = statistics.mean(vals)
     sample = (f"oracle epoch (oracle/gcn.py fp64, p=1) on {args.config}: dense ops full size, "
               f"each SpMM on a {args.cpu_frac:.0%} row sample scaled by {1 / args.cpu_frac:.0f}")
@@ -288,12 +297,15 @@ def main(args):
         return 0
     peaks, src = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
+    sp_ld = stats[-1]["spmm_ld"]
+    sp_c = sum(st["spmm_bytes_compulsory"] for st in stats)
     achieved = (sp_bytes / (sp_ms * 1e-3) / 1e9) if sp_ms > 0 else None
+    avg_launch_ms = sp_ms / sp_n if sp_n else None
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"{args.config}_p{world}_spmm")
+            traffic = json.load(open(tpath)).get(f"{args.config}_p{world}_{args.mode}_spmm_ld{sp_ld}")
         except Exception:
             traffic = None
     out = {
@@ -314,11 +326,16 @@ def main(args):
                    if ms_sync_max > 0 and max_wire > 0 else None},
         "phase_ms": {"gemm": round(ms_gemm, 3), "spmm": round(ms_spmm, 3), "sync": round(ms_sync, 3)},
         "loss": stats[-1]["loss"], "train_acc": stats[-1]["acc"], "eps": stats[-1]["eps_used"],
-        "roofline": {"kernel": "spmm", "bound": "hbm",
+        "roofline": {"kernel": f"spmm (ld={sp_ld}, the dominant launch group)", "bound": "hbm",
                      "achieved": round(achieved, 1) if achieved else None, "peak": hbm,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4) if achieved else None,
-                     "peak_source": src, "traffic": traffic,
-                     "bytes_model": "gather model: 4(n+1) + 8 nnz + 4 ld nnz + 4 ld n per launch",
+                     "traffic": traffic, "peak_source": src,
+                     "bytes_model": "gather model per launch: 4(n+1) + 8 nnz + 4 ld nnz + 4 ld n",
+                     "bytes_per_launch": round(sp_bytes / sp_n) if sp_n else None,
+                     "compulsory_bytes_per_launch": round(sp_c / sp_n) if sp_n else None,
+                     "avg_launch_ms": round(avg_launch_ms, 4) if avg_launch_ms else None,
+                     "dram_gbs": round(traffic / (avg_launch_ms * 1e-3) / 1e9, 1)
+                     if (traffic and avg_launch_ms) else None,
                      "launches": sp_n},
         "gpu_launches": launches,
         "prep_s": round(t_prep, 1),
@@ -328,7 +345,7 @@ def main(args):
     if clk:
         out["clocks"] = clk
     if world == 1 and not args.no_cpu_baseline:
-        v = oracle_epoch_cost(ds, args.cpu_frac)
+        v = OracleSample(ds, args.cpu_frac).epoch_ms()
         out["cpu_baseline"] = {
             "value": round(v, 1), "unit": "ms", "cores": cpu_cores(), "kind": "oracle",
             "sample": f"oracle/gcn.py epoch (fp64, p=1): dense ops full size, each SpMM on a "

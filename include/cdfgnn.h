@@ -212,9 +212,12 @@ typedef struct {
     int32_t gpu_launches;       /* kernels this library launched in the epoch */
     /* cfg.timing = 1: CUDA-event milliseconds per phase (summed over calls) */
     double ms_gemm, ms_spmm, ms_sync, ms_other;
-    int32_t spmm_launches;
-    double spmm_bytes;          /* algorithmic bytes of the SpMM launches */
-    double spmm_ms_sum;         /* summed SpMM launch time */
+    /* the dominant SpMM width (largest summed time) of this epoch: */
+    int32_t spmm_ld;            /* its row width ld */
+    int32_t spmm_launches;      /* its launches */
+    double spmm_bytes;          /* their gather-model bytes */
+    double spmm_bytes_compulsory;   /* their compulsory bytes */
+    double spmm_ms_sum;         /* their summed CUDA-event time */
 } cdfgnn_epoch_stats;
 
 /* Alg. 1 once.  X[k] device (n_i x ld(F_0)), labels[k] int32 [n_i],

@@ -81,7 +81,8 @@ class EpochStatsC(ctypes.Structure):
                 ("eps_used", c_f64), ("eps_next", c_f64), ("fwd", SyncStatsC * MAX_LAYERS),
                 ("bwd", SyncStatsC * MAX_LAYERS), ("gpu_launches", c_i32), ("ms_gemm", c_f64),
                 ("ms_spmm", c_f64), ("ms_sync", c_f64), ("ms_other", c_f64),
-                ("spmm_launches", c_i32), ("spmm_bytes", c_f64), ("spmm_ms_sum", c_f64)]
+                ("spmm_ld", c_i32), ("spmm_launches", c_i32), ("spmm_bytes", c_f64),
+                ("spmm_bytes_compulsory", c_f64), ("spmm_ms_sum", c_f64)]
 
 
 def _sig(name, res, args):

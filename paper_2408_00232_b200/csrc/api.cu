@@ -124,6 +124,7 @@ struct cdfgnn_ctx {
     bool timing = false;
     std::vector<cudaEvent_t> ev;
     std::vector<int> ev_phase;
+    std::vector<int64_t> ev_tag;   // SpMM: row width ld of the launch
     size_t ev_used = 0;
     size_t ws_bytes = 0;
     void* ws = nullptr;
@@ -251,16 +252,18 @@ void carve(cdfgnn_ctx* c, Bump& b) {
 }
 
 // ---- phase timing ----------------------------------------------------------------
-void mark(cdfgnn_ctx* c, int phase, cudaStream_t s) {
+void mark(cdfgnn_ctx* c, int phase, cudaStream_t s, int64_t tag = 0) {
     if (!c->timing) return;
     if (c->ev_used >= c->ev.size()) {
         cudaEvent_t e;
         if (cudaEventCreate(&e) != cudaSuccess) return;
         c->ev.push_back(e);
         c->ev_phase.push_back(0);
+        c->ev_tag.push_back(0);
     }
     cudaEventRecord(c->ev[c->ev_used], s);
     c->ev_phase[c->ev_used] = phase;
+    c->ev_tag[c->ev_used] = tag;
     c->ev_used++;
 }
 
@@ -463,7 +466,7 @@ int read_stats_now(cdfgnn_ctx* c, int l, int dir, int64_t wire, cudaStream_t s,
 }
 
 int spmm_part(cdfgnn_ctx* c, LocalPart& P, const float* T, float* Y, int64_t ld, cudaStream_t s) {
-    mark(c, PH_SPMM, s);
+    mark(c, PH_SPMM, s, ld);
     launch_spmm(P.rowptr, P.colidx, P.val, P.n, T, Y, ld, s);
     c->launches++;
     return check_launch("spmm");
@@ -801,27 +804,40 @@ static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const
         out->gpu_launches = c->launches;
         if (c->timing && c->ev_used >= 2) {
             double ph[5] = {0, 0, 0, 0, 0};
-            int nsp = 0;
-            double spsum = 0;
+            std::vector<std::pair<int64_t, std::pair<int, double>>> per;   // ld -> (launches, ms)
             for (size_t e = 0; e + 1 < c->ev_used; ++e) {
                 float ms = 0.f;
                 cudaEventElapsedTime(&ms, c->ev[e], c->ev[e + 1]);
                 ph[c->ev_phase[e]] += ms;
-                if (c->ev_phase[e] == PH_SPMM) { nsp++; spsum += ms; }
+                if (c->ev_phase[e] == PH_SPMM) {
+                    bool found = false;
+                    for (auto& q : per)
+                        if (q.first == c->ev_tag[e]) { q.second.first++; q.second.second += ms; found = true; }
+                    if (!found) per.push_back({c->ev_tag[e], {1, (double)ms}});
+                }
             }
             out->ms_gemm = ph[PH_GEMM];
             out->ms_spmm = ph[PH_SPMM];
             out->ms_sync = ph[PH_SYNC];
             out->ms_other = ph[PH_OTHER];
-            out->spmm_launches = nsp;
-            out->spmm_ms_sum = spsum;
-            double bytes = 0;
-            for (int l = 1; l <= L; ++l) {
-                const double ld = (double)ld_of(c->cfg.dims[l]);
-                for (const LocalPart& P : c->parts)   // fwd + bwd SpMM at width F_l
-                    bytes += 2.0 * (4.0 * (P.n + 1) + 8.0 * P.nnz + 4.0 * ld * P.nnz + 4.0 * ld * P.n);
+            size_t best = 0;
+            for (size_t q = 1; q < per.size(); ++q)
+                if (per[q].second.second > per[best].second.second) best = q;
+            if (!per.empty()) {
+                const double ld = (double)per[best].first;
+                out->spmm_ld = (int32_t)per[best].first;
+                out->spmm_launches = per[best].second.first;
+                out->spmm_ms_sum = per[best].second.second;
+                // every part launches each width once per direction: bytes per launch averaged
+                double g = 0, cpl = 0;
+                for (const LocalPart& P : c->parts) {
+                    g += 4.0 * (P.n + 1) + 8.0 * P.nnz + 4.0 * ld * P.nnz + 4.0 * ld * P.n;
+                    cpl += 4.0 * (P.n + 1) + 8.0 * P.nnz + 4.0 * ld * P.n + 4.0 * ld * P.n;
+                }
+                const double per_launch = g / c->k, per_launch_c = cpl / c->k;
+                out->spmm_bytes = per_launch * out->spmm_launches;
+                out->spmm_bytes_compulsory = per_launch_c * out->spmm_launches;
             }
-            out->spmm_bytes = bytes;
         }
     }
     // ε controller (R17, R18): first epoch seeds mean_acc without changing ε
