@@ -1,0 +1,83 @@
+"""Multi-GPU parity check (run under torchrun, one rank per GPU, NCCL).
+
+Every rank trains its own partition (world = p) for E epochs; rank 0 also runs the
+same p parts co-resident on its GPU (world = 1, in-device exchange).  The two
+trajectories must agree (loss 1e-5 relative, counters identical in exact mode),
+and W must be bit-identical on every rank.
+    torchrun --nproc-per-node N tools/mgpu_check.py [--config C2] [--epochs 5]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="")
+    ap.add_argument("--epochs", type=int, default=5)
+    ap.add_argument("--mode", default="cache_int8")
+    a = ap.parse_args()
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2408_00232_b200.runtime import Run
+    from synth import get_config, make_dataset, small_random_graph
+    if a.config:
+        ds = make_dataset(get_config(a.config))
+    else:
+        ds = small_random_graph(3000, 20000, (24, 32, 6), seed=71)
+    cache, quant = {"cache_int8": (True, 8), "cache_fp32": (True, 0), "nocache": (False, 0),
+                    "exact": (True, 0)}[a.mode]
+    eps0 = 0.0 if a.mode == "exact" else 0.01
+    kw = dict(cache=cache, quant_bits=quant, eps0=eps0, adaptive=a.mode != "exact",
+              optimizer="adam", lr=0.01)
+    run = Run(ds, world, rank=rank, world=world, device=local, **kw)
+    ref = Run(ds, world, device=local, plan=run.plan, **kw) if rank == 0 else None
+    ok = True
+    rows = []
+    for ep in range(a.epochs):
+        g = run.epoch()
+        # bit-identical replicated W across ranks
+        flat = torch.cat([w.flatten() for w in run.W])
+        allw = [torch.empty_like(flat) for _ in range(world)]
+        dist.all_gather(allw, flat)
+        same = all(torch.equal(allw[0], x) for x in allw)
+        sent = torch.tensor([sum(s["gather_sent"] + s["scatter_msgs"] for s in g["fwd"] + g["bwd"])],
+                            dtype=torch.int64, device="cuda")
+        dist.all_reduce(sent)
+        if rank == 0:
+            r = ref.epoch()
+            rsent = sum(s["gather_sent"] + s["scatter_msgs"] for s in r["fwd"] + r["bwd"])
+            rel = abs(g["loss"] - r["loss"]) / max(1.0, abs(r["loss"]))
+            row = dict(epoch=ep, loss=g["loss"], loss_1gpu=r["loss"], rel=rel, w_same=bool(same),
+                       msgs=int(sent.item()), msgs_1gpu=rsent, eps=g["eps_used"],
+                       wire=sum(s["bytes_wire"] for s in g["fwd"] + g["bwd"]))
+            rows.append(row)
+            print(json.dumps(row), flush=True)
+            tol = 1e-5 if a.mode == "exact" else 2e-3
+            if rel > tol or not same:
+                ok = False
+            if a.mode == "exact" and row["msgs"] != rsent:
+                ok = False
+    if rank == 0:
+        print(json.dumps({"mgpu_check": "PASS" if ok else "FAIL", "world": world, "mode": a.mode}),
+              flush=True)
+    run.close()
+    if ref:
+        ref.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0 if ok else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
