@@ -142,7 +142,8 @@ typedef struct {
     int32_t quant_bits;                 /* 0 (fp32 payloads) or 8 (uint8 codes), §5 */
     int32_t optimizer;                  /* 0 SGD, 1 Adam */
     double lr, beta1, beta2, adam_eps;
-    int32_t gemm_tf32;                  /* 1: tcgen05 kind::tf32 GEMMs; 0: fp32 SIMT GEMMs */
+    int32_t gemm_tf32;                  /* 3: tcgen05 3xTF32 GEMMs (default, ~fp32 accuracy);
+                                           1: tcgen05 1xTF32; 0: fp32 SIMT GEMMs */
     int32_t timing;                     /* 1: per-phase CUDA-event timing in epoch stats */
 } cdfgnn_cfg;
 

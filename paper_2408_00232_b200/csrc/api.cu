@@ -111,6 +111,12 @@ struct cdfgnn_ctx {
     int64_t woff[CDFGNN_MAX_LAYERS + 1] = {};
     int64_t splitk_cap = 0;
     float *dW = nullptr, *adam_m = nullptr, *adam_v = nullptr, *splitk = nullptr;
+    float* wpad = nullptr;             // W^(l) with zero-padded rows of ld(F_l) (TMA strides)
+    int64_t wpoff[CDFGNN_MAX_LAYERS + 1] = {};
+    float* wtpad = nullptr;            // W^(l)ᵀ [F_l x ld(F_{l-1})] (K-major B of T = H W)
+    int64_t wtoff[CDFGNN_MAX_LAYERS + 1] = {};
+    float *trA = nullptr, *trB = nullptr;   // K-major copies Hᵀ, Sᵀ for ∇W (tcgen05 path)
+    int64_t npad = 0, fin_max = 0;
     unsigned long long* stats_d = nullptr;    // [L][2][4]
     unsigned long long* stats_h = nullptr;    // pinned
     double* loss_d = nullptr;        // [k]
@@ -159,6 +165,19 @@ int prepare(cdfgnn_ctx* c, const cdfgnn_plan* plan, const int32_t* parts, int32_
         c->wtotal += (int64_t)cfg->dims[l - 1] * cfg->dims[l];
     }
     c->woff[cfg->L] = c->wtotal;
+    int64_t wp = 0;
+    for (int l = 1; l <= cfg->L; ++l) {
+        c->wpoff[l - 1] = wp;
+        wp += align_up((int64_t)cfg->dims[l - 1] * ld_of(cfg->dims[l]), 64);
+    }
+    c->wpoff[cfg->L] = wp;
+    int64_t wt = 0;
+    for (int l = 1; l <= cfg->L; ++l) {
+        c->wtoff[l - 1] = wt;
+        wt += align_up((int64_t)cfg->dims[l] * ld_of(cfg->dims[l - 1]), 64);
+        c->fin_max = std::max<int64_t>(c->fin_max, cfg->dims[l - 1]);
+    }
+    c->wtoff[cfg->L] = wt;
     int64_t maxw = 0;
     for (int l = 1; l <= cfg->L; ++l) maxw = std::max<int64_t>(maxw, (int64_t)cfg->dims[l - 1] * cfg->dims[l]);
     c->splitk_cap = 64 * maxw;
@@ -246,6 +265,15 @@ void carve(cdfgnn_ctx* c, Bump& b) {
     c->adam_m = b.take<float>(c->wtotal);
     c->adam_v = b.take<float>(c->wtotal);
     c->splitk = b.take<float>(c->splitk_cap);
+    c->wpad = b.take<float>(c->wpoff[c->cfg.L]);
+    c->wtpad = b.take<float>(c->wtoff[c->cfg.L]);
+    int64_t nmax = 0;
+    for (const LocalPart& P : c->parts) nmax = std::max(nmax, P.n);
+    c->npad = ld_of(nmax);
+    if (c->cfg.gemm_tf32) {
+        c->trA = b.take<float>(c->fin_max * c->npad);
+        c->trB = b.take<float>(c->Fmax * c->npad);
+    }
     c->stats_d = b.take<unsigned long long>(CDFGNN_MAX_LAYERS * 2 * 4);
     c->loss_d = b.take<double>(std::max(c->k, 1));
     c->scal_d = b.take<int32_t>(8);
@@ -477,11 +505,21 @@ int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, cons
              int64_t* wire) {
     const int64_t Fi = c->cfg.dims[l - 1], Fo = c->cfg.dims[l];
     if (ld_in < Fi || ld_in % 4 || ld_out != ld_of(Fo)) CDF_FAIL(CDFGNN_EUSAGE, "bad leading dimension");
+    float* Wt = c->wtpad + c->wtoff[l - 1];
+    const int64_t ldwt = ld_of(Fi);
+    if (c->cfg.gemm_tf32) {
+        mark(c, PH_GEMM, s);
+        c->launches += launch_transpose(W, Fi, Fo, Fo, Wt, ldwt, s);
+    }
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
         mark(c, PH_GEMM, s);
-        launch_gemm_simt(false, false, P.n, Fo, Fi, H_in[t], ld_in, W, Fo, P.T, ld_out, nullptr, 0,
-                         nullptr, 0, false, s);
+        if (c->cfg.gemm_tf32) {
+            CDF_TRY(gemm_tc_fwd(P.n, Fo, Fi, H_in[t], ld_in, Wt, ldwt, P.T, ld_out, c->cfg.gemm_tf32 == 3, s));
+        } else {
+            launch_gemm_simt(false, false, P.n, Fo, Fi, H_in[t], ld_in, W, Fo, P.T, ld_out, nullptr, 0,
+                             nullptr, 0, false, s);
+        }
         c->launches++;
         CDF_TRY(check_launch("gemm fwd"));
         CDF_TRY(spmm_part(c, P, P.T, Z[t], ld_out, s));
@@ -509,13 +547,26 @@ int bwd_impl(cdfgnn_ctx* c, int l, float* const* dZ, int64_t ld, const float* co
         CDF_TRY(spmm_part(c, P, dZ[t], P.S, ld, s));
         mark(c, PH_GEMM, s);
         // dW (+)= H_inᵀ S ; parts accumulate in ascending order
-        launch_gemm_simt(true, false, Fi, Fo, P.n, H_in[t], ld_in, P.S, ld, dW, Fo, nullptr, 0,
-                         c->splitk, c->splitk_cap, t > 0, s);
-        c->launches += 2;
-        if (dZ_prev) {
-            launch_gemm_simt(false, true, P.n, Fi, Fo, P.S, ld, W, Fo, dZ_prev[t], ld_in, H_in[t],
-                             ld_in, nullptr, 0, false, s);
-            c->launches++;
+        if (c->cfg.gemm_tf32) {
+            if (t == 0) c->launches += launch_pad_rows(W, Fi, Fo, c->wpad + c->wpoff[l - 1], ld, s);
+            c->launches += launch_transpose(H_in[t], P.n, Fi, ld_in, c->trA, c->npad, s);
+            c->launches += launch_transpose(P.S, P.n, Fo, ld, c->trB, c->npad, s);
+            CDF_TRY(gemm_tc_wgrad(Fi, Fo, P.n, c->trA, c->npad, c->trB, c->npad, dW, Fo, c->splitk,
+                                  c->splitk_cap, t > 0, c->cfg.gemm_tf32 == 3, s, &c->launches));
+            if (dZ_prev) {
+                CDF_TRY(gemm_tc_bwd_data(P.n, Fi, Fo, P.S, ld, c->wpad + c->wpoff[l - 1], ld, dZ_prev[t],
+                                         ld_in, H_in[t], ld_in, c->cfg.gemm_tf32 == 3, s));
+                c->launches++;
+            }
+        } else {
+            launch_gemm_simt(true, false, Fi, Fo, P.n, H_in[t], ld_in, P.S, ld, dW, Fo, nullptr, 0,
+                             c->splitk, c->splitk_cap, t > 0, s);
+            c->launches += 2;
+            if (dZ_prev) {
+                launch_gemm_simt(false, true, P.n, Fi, Fo, P.S, ld, W, Fo, dZ_prev[t], ld_in, H_in[t],
+                                 ld_in, nullptr, 0, false, s);
+                c->launches++;
+            }
         }
         CDF_TRY(check_launch("gemm bwd"));
     }
@@ -547,7 +598,7 @@ extern "C" int cdfgnn_cfg_default(cdfgnn_cfg* cfg) {
     cfg->quant_bits = 8;
     cfg->optimizer = 1;
     cfg->lr = 0.01; cfg->beta1 = 0.9; cfg->beta2 = 0.999; cfg->adam_eps = 1e-8;
-    cfg->gemm_tf32 = 0;
+    cfg->gemm_tf32 = 3;
     cfg->timing = 0;
     return CDFGNN_OK;
 }

@@ -1,0 +1,514 @@
+// tcgen05 TF32 tensor-core GEMMs for the dense feature transform and its gradients.
+//
+//   T  = H W                  (eq. 1; R5 Â(HW))        A = H,  B = Wᵀ (padded copy)
+//   δ̈  = (S Wᵀ) ⊙ 𝟙[H > 0]    (R3, R6)              A = S,  B = W  (padded copy)
+//   ∇W = Hᵀ S                 (eq. 5; R6), split-K  A = Hᵀ, B = Sᵀ (transposed copies)
+// Every operand is fed K-major: on sm_100a the tf32 MMA with an MN-major operand
+// descriptor returned zeros in our tests (tools/tc_debug.cu), so the two
+// vertex-major operands of ∇W are transposed into K-major scratch first.
+//
+// One CTA computes a 128 x BN fp32 tile over a K range: warp 0 issues TMA loads
+// (128-byte swizzled boxes, fp32 -> tf32 rounding in the tensor map) into a
+// STAGES-deep shared-memory ring guarded by mbarriers; one elected thread of
+// warp 1 issues tcgen05.mma.cta_group::1.kind::tf32 (M = 128, N = BN, K = 8) with
+// the accumulator in TMEM and tcgen05.commit releasing ring slots; warps 2-5 read
+// the accumulator with tcgen05.ld (32 lanes each) and run the epilogue (mask,
+// zero padding columns, split-K partials).  Split-K partials are summed in a
+// fixed order by a separate kernel, so results are run-to-run deterministic.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+
+#include "common.h"
+#include "kernels.h"
+
+namespace cdfgnn {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 32;            // 32 tf32 = 128 bytes: one swizzle row
+constexpr int kThreads = 192;     // 6 warps: TMA, MMA, 4 x epilogue
+#ifndef GEMM_MN_LBO
+#define GEMM_MN_LBO (BK * 128)   // MN-major: byte stride between 32-element MN chunks
+#endif
+#ifndef GEMM_MN_SBO
+#define GEMM_MN_SBO 1024         // MN-major: byte stride between groups of 8 k-rows
+#endif
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// 128-byte-swizzled shared-memory matrix descriptor (sm_100 UMMA, version 1)
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;          // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;          // SWIZZLE_128B
+    return d;
+}
+
+// 32 lanes x 32 consecutive 32-bit TMEM columns -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int BN, bool SPLIT3>
+struct Cfg {
+    static constexpr int A_BYTES = BM * BK * 4;
+    static constexpr int B_BYTES = BN * BK * 4;
+    static constexpr int TMA_BYTES = A_BYTES + B_BYTES;                  // fp32 (or tf32) tiles
+    static constexpr int STAGE_BYTES = TMA_BYTES * (SPLIT3 ? 2 : 1);     // + lo parts for 3xTF32
+    static constexpr int STAGES = (SPLIT3 ? 196608 : 200704) / STAGE_BYTES;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+};
+
+__device__ __forceinline__ float tf32_rn(float x) {
+    uint32_t u = __float_as_uint(x);
+    u = (u + 0xFFFu + ((u >> 13) & 1u)) & ~0x1FFFu;      // round to nearest even, 10-bit mantissa
+    return __uint_as_float(u);
+}
+
+struct EpiArgs {
+    float* C;          // output (or nullptr with ws)
+    int64_t ldc;
+    const float* mask; // optional: C *= (mask > 0)
+    int64_t ldm;
+    float* ws;         // split-K partials [z][M][ldw]
+    int64_t ldw;
+    int accumulate;
+};
+
+template <bool A_MN, bool B_MN, int BN, bool SPLIT3>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                 int total_kb, int kb_per_split, EpiArgs ep) {
+    using C_ = Cfg<BN, SPLIT3>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // stage s: [A (hi)][B (hi)][A lo][B lo]   (lo parts only with SPLIT3)
+    auto stA = [&](int st) { return smem + st * C_::STAGE_BYTES; };
+    auto stB = [&](int st) { return smem + st * C_::STAGE_BYTES + C_::A_BYTES; };
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C_::STAGES * C_::STAGE_BYTES);
+    uint64_t* empty = full + C_::STAGES;
+    uint64_t* conv = empty + C_::STAGES;
+    uint64_t* tmem_full = conv + C_::STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    const int kb0 = blockIdx.z * kb_per_split;
+    const int kb1 = min(total_kb, kb0 + kb_per_split);
+    const int nkb = kb1 - kb0;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < C_::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+            mbar_init(&conv[s], 4);          // one arrival per converter warp
+        }
+        mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(C_::TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer ----------------
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % C_::STAGES;
+                const uint32_t ph = (uint32_t)(i / C_::STAGES) & 1u;
+                mbar_wait(&empty[s], ph ^ 1u);
+                mbar_expect_tx(&full[s], C_::TMA_BYTES);
+                const int k = (kb0 + i) * BK;
+                uint8_t* a = stA(s);
+                uint8_t* b = stB(s);
+                if (!A_MN) {
+                    tma_load_2d(a, &tmA, &full[s], k, m0);                         // box {32 k, 128 m}
+                } else {
+#pragma unroll
+                    for (int c = 0; c < BM / 32; ++c)                               // box {32 m, 32 k}
+                        tma_load_2d(a + c * BK * 128, &tmA, &full[s], m0 + 32 * c, k);
+                }
+                if (!B_MN) {
+                    tma_load_2d(b, &tmB, &full[s], k, n0);                         // box {32 k, BN n}
+                } else {
+#pragma unroll
+                    for (int c = 0; c < BN / 32; ++c)                               // box {32 n, 32 k}
+                        tma_load_2d(b + c * BK * 128, &tmB, &full[s], n0 + 32 * c, k);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer ----------------
+            constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                                       ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                                       ((uint32_t)(BM >> 4) << 24);
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % C_::STAGES;
+                const uint32_t ph = (uint32_t)(i / C_::STAGES) & 1u;
+                mbar_wait(SPLIT3 ? &conv[s] : &full[s], ph);
+                tc_fence_after();
+                const uint32_t a_base = smem_u32(stA(s));
+                const uint32_t b_base = smem_u32(stB(s));
+                if (SPLIT3) {
+                    // 3xTF32: A_hi·B_hi + A_hi·B_lo + A_lo·B_hi
+                    const uint32_t alo = a_base + C_::TMA_BYTES, blo = b_base + C_::TMA_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 8; ++kk) {
+                        const uint64_t ah = smem_desc(a_base + kk * 32, 16, 1024);
+                        const uint64_t bh = smem_desc(b_base + kk * 32, 16, 1024);
+                        const uint64_t al = smem_desc(alo + kk * 32, 16, 1024);
+                        const uint64_t bl = smem_desc(blo + kk * 32, 16, 1024);
+                        tc_mma_tf32(tmem, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                        tc_mma_tf32(tmem, ah, bl, idesc, 1u);
+                        tc_mma_tf32(tmem, al, bh, idesc, 1u);
+                    }
+                    tc_commit(&empty[s]);
+                    continue;
+                }
+#pragma unroll
+                for (int kk = 0; kk < BK / 8; ++kk) {
+                    // K-major: +32 B per 8 tf32 inside the 128-B swizzle row (LBO unused, SBO = 8 rows)
+                    // MN-major: +1024 B per 8 k-rows (LBO = stride of 32-wide MN chunks, SBO = 8 rows)
+                    const uint64_t ad = A_MN ? smem_desc(a_base + kk * 1024, GEMM_MN_LBO, GEMM_MN_SBO)
+                                             : smem_desc(a_base + kk * 32, 16, 1024);
+                    const uint64_t bd = B_MN ? smem_desc(b_base + kk * 1024, GEMM_MN_LBO, GEMM_MN_SBO)
+                                             : smem_desc(b_base + kk * 32, 16, 1024);
+                    tc_mma_tf32(tmem, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                }
+                tc_commit(&empty[s]);       // slot free once these MMAs have read it
+            }
+            tc_commit(tmem_full);           // accumulator complete
+        }
+    } else {
+        if (SPLIT3) {
+            // ---------------- converters: fp32 -> tf32 hi + lo (in place + lo buffer) ----------------
+            const int ct = threadIdx.x - 64;                 // 0..127
+            constexpr int NV = C_::TMA_BYTES / 16;           // float4 per stage (A and B)
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % C_::STAGES;
+                const uint32_t ph = (uint32_t)(i / C_::STAGES) & 1u;
+                mbar_wait(&full[s], ph);
+                float4* base = reinterpret_cast<float4*>(stA(s));
+                float4* lo = reinterpret_cast<float4*>(stA(s) + C_::TMA_BYTES);
+#pragma unroll 4
+                for (int v = ct; v < NV; v += 128) {
+                    const float4 x = base[v];
+                    float4 h, l;
+                    h.x = tf32_rn(x.x); h.y = tf32_rn(x.y); h.z = tf32_rn(x.z); h.w = tf32_rn(x.w);
+                    l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+                    base[v] = h;
+                    lo[v] = l;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to tcgen05
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&conv[s])) : "memory");
+            }
+        }
+        // ---------------- epilogue: warps 2..5 ----------------
+        const int q = warp & 3;             // TMEM lane quarter this warp may access
+        const int row = m0 + 32 * q + lane;
+        if (nkb > 0) {
+            mbar_wait(tmem_full, 0);
+            tc_fence_after();
+        }
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+            float v[32];
+            if (nkb > 0) {
+                tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0, v);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = 0.f;
+            }
+            if (row >= M) continue;
+            const int col0 = n0 + c0;
+            if (ep.ws) {
+                float* w = ep.ws + ((int64_t)blockIdx.z * M + row) * ep.ldw;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (col0 + j < ep.ldw) w[col0 + j] = (col0 + j < N) ? v[j] : 0.f;
+                continue;
+            }
+            float* crow = ep.C + (int64_t)row * ep.ldc;
+            const float* mrow = ep.mask ? ep.mask + (int64_t)row * ep.ldm : nullptr;
+            const bool full_chunk = (col0 + 32 <= N) && ((ep.ldc & 3) == 0) && !ep.accumulate;
+            if (full_chunk) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                    float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    if (mrow) {
+                        const float4 mk = *reinterpret_cast<const float4*>(mrow + col0 + j);
+                        if (!(mk.x > 0.f)) o.x = 0.f;
+                        if (!(mk.y > 0.f)) o.y = 0.f;
+                        if (!(mk.z > 0.f)) o.z = 0.f;
+                        if (!(mk.w > 0.f)) o.w = 0.f;
+                    }
+                    *reinterpret_cast<float4*>(crow + col0 + j) = o;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int col = col0 + j;
+                    if (col >= ep.ldc) break;
+                    float o = col < N ? v[j] : 0.f;
+                    if (mrow && col < N && !(mrow[col] > 0.f)) o = 0.f;
+                    if (ep.accumulate && col < N) o += crow[col];
+                    crow[col] = o;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C_::TMEM_COLS)
+                     : "memory");
+    }
+}
+
+__global__ void splitk_sum_kernel(int64_t M, int64_t N, int64_t ldw, int splits, const float* __restrict__ ws,
+                                  float* __restrict__ C, int64_t ldc, int accumulate) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M * ldc) return;
+    const int64_t m = i / ldc, n = i % ldc;
+    if (n >= N) { C[i] = 0.f; return; }
+    float v = 0.f;
+    for (int z = 0; z < splits; ++z) v += ws[((int64_t)z * M + m) * ldw + n];   // fixed order
+    if (accumulate) v += C[i];
+    C[i] = v;
+}
+
+// dst[c][r] = src[r][c]  (r < rows, c < cols), 32 x 32 tiles through shared memory
+__global__ void transpose_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+                                 float* __restrict__ dst, int64_t ldd) {
+    __shared__ float tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        tile[i][threadIdx.x] = (r < rows && c < cols) ? src[r * lds + c] : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (c < cols && r < rows) dst[c * ldd + r] = tile[threadIdx.x][i];
+    }
+}
+
+__global__ void pad_rows_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, float* __restrict__ dst,
+                                int64_t ldd) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= rows * ldd) return;
+    const int64_t r = i / ldd, c = i % ldd;
+    dst[i] = c < cols ? src[r * cols + c] : 0.f;
+}
+
+// ---- host: tensor maps ----------------------------------------------------------
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    }
+    return fn;
+}
+
+// 2-D fp32 row-major matrix [rows x cols] with row stride ld (elements); box {bc, br}
+bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld, int bc, int br,
+              bool raw_fp32 = false) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+    cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, raw_fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_TFLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <bool A_MN, bool B_MN, int BN, bool SPLIT3>
+int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, int64_t M, int64_t N, int64_t K, int splits,
+                   const EpiArgs& ep, cudaStream_t s) {
+    using C_ = Cfg<BN, SPLIT3>;
+    static bool attr = false;
+    auto kern = gemm_tf32_kernel<A_MN, B_MN, BN, SPLIT3>;
+    if (!attr) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM) != cudaSuccess)
+            return CDFGNN_ECUDA;
+        attr = true;
+    }
+    const int total_kb = (int)((K + BK - 1) / BK);
+    const int kbps = (total_kb + splits - 1) / splits;
+    const int zs = (total_kb + kbps - 1) / kbps;
+    dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), (unsigned)std::max(zs, 1));
+    kern<<<grid, kThreads, C_::SMEM, s>>>(ta, tb, (int)M, (int)N, total_kb, kbps, ep);
+    return cudaGetLastError() == cudaSuccess ? CDFGNN_OK : CDFGNN_ECUDA;
+}
+
+template <bool A_MN, bool B_MN>
+int launch_bn(int BN, bool split3, const CUtensorMap& ta, const CUtensorMap& tb, int64_t M, int64_t N, int64_t K,
+              int splits, const EpiArgs& ep, cudaStream_t s) {
+    if (split3) {
+        if (BN == 64) return launch_variant<A_MN, B_MN, 64, true>(ta, tb, M, N, K, splits, ep, s);
+        return launch_variant<A_MN, B_MN, 128, true>(ta, tb, M, N, K, splits, ep, s);
+    }
+    if (BN == 64) return launch_variant<A_MN, B_MN, 64, false>(ta, tb, M, N, K, splits, ep, s);
+    if (BN == 128) return launch_variant<A_MN, B_MN, 128, false>(ta, tb, M, N, K, splits, ep, s);
+    return launch_variant<A_MN, B_MN, 256, false>(ta, tb, M, N, K, splits, ep, s);
+}
+
+int pick_bn(int64_t N, bool split3) { return N <= 64 ? 64 : ((N <= 128 || split3) ? 128 : 256); }
+
+}  // namespace
+
+int launch_transpose(const float* src, int64_t rows, int64_t cols, int64_t lds, float* dst, int64_t ldd,
+                     cudaStream_t s) {
+    if (rows <= 0 || cols <= 0) return 0;
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+    transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, lds, dst, ldd);
+    return 1;
+}
+
+int launch_pad_rows(const float* src, int64_t rows, int64_t cols, float* dst, int64_t ldd, cudaStream_t s) {
+    const int64_t tot = rows * ldd;
+    if (tot <= 0) return 0;
+    pad_rows_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(src, rows, cols, dst, ldd);
+    return 1;
+}
+
+// T[M x ldc] = A[M x K] (lda) · Btᵀ with Bt = Wᵀ given as [N x K] (row stride ldb)   (zero pad columns)
+int gemm_tc_fwd(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* Bt, int64_t ldb, float* C,
+                int64_t ldc, bool split3, cudaStream_t s) {
+    const int BN = pick_bn(std::max(N, ldc), split3);
+    CUtensorMap ta, tb;
+    if (!make_map(&ta, A, M, K, lda, BK, BM, split3) || !make_map(&tb, Bt, N, K, ldb, BK, BN, split3))
+        CDF_FAIL(CDFGNN_ECUDA, "cuTensorMapEncodeTiled failed (fwd)");
+    EpiArgs ep{C, ldc, nullptr, 0, nullptr, 0, 0};
+    return launch_bn<false, false>(BN, split3, ta, tb, M, N, K, 1, ep, s);
+}
+
+// C[M x ldc] = (A[M x K] (lda) · Bᵀ) ⊙ 𝟙[mask > 0], B given as [N x K] (row stride ldb, K-major)
+int gemm_tc_bwd_data(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* Bk, int64_t ldb,
+                     float* C, int64_t ldc, const float* mask, int64_t ldm, bool split3, cudaStream_t s) {
+    const int BN = pick_bn(std::max(N, ldc), split3);
+    CUtensorMap ta, tb;
+    if (!make_map(&ta, A, M, K, lda, BK, BM, split3) || !make_map(&tb, Bk, N, K, ldb, BK, BN, split3))
+        CDF_FAIL(CDFGNN_ECUDA, "cuTensorMapEncodeTiled failed (bwd data)");
+    EpiArgs ep{C, ldc, mask, ldm, nullptr, 0, 0};
+    return launch_bn<false, false>(BN, split3, ta, tb, M, N, K, 1, ep, s);
+}
+
+// C[M x N] (+)= Ht · Stᵀ with Ht = Hᵀ [M x K] (ldh) and St = Sᵀ [N x K] (lds), K = vertices; split-K
+int gemm_tc_wgrad(int64_t M, int64_t N, int64_t K, const float* Ht, int64_t ldh, const float* St, int64_t lds,
+                  float* C, int64_t ldc, float* ws, int64_t ws_cap, bool accumulate, bool split3, cudaStream_t s,
+                  int* launches) {
+    const int BN = pick_bn(N, split3);
+    CUtensorMap ta, tb;
+    if (!make_map(&ta, Ht, M, K, ldh, BK, BM, split3) || !make_map(&tb, St, N, K, lds, BK, BN, split3))
+        CDF_FAIL(CDFGNN_ECUDA, "cuTensorMapEncodeTiled failed (wgrad)");
+    const int64_t ldw = (N + 3) / 4 * 4;
+    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    const int64_t total_kb = (K + BK - 1) / BK;
+    int64_t splits = std::max<int64_t>(1, std::min<int64_t>(2 * 148 / std::max<int64_t>(tiles, 1), total_kb / 8));
+    while (splits > 1 && splits * M * ldw > ws_cap) splits--;
+    const int kbps = (int)((total_kb + splits - 1) / splits);
+    const int zs = (int)((total_kb + kbps - 1) / kbps);
+    EpiArgs ep{nullptr, 0, nullptr, 0, ws, ldw, 0};
+    int rc = launch_bn<false, false>(BN, split3, ta, tb, M, N, K, (int)splits, ep, s);
+    if (rc != CDFGNN_OK) CDF_FAIL(rc, "wgrad launch failed");
+    const int64_t tot = M * ldc;
+    splitk_sum_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(M, N, ldw, zs, ws, C, ldc, accumulate ? 1 : 0);
+    if (launches) *launches += 2;
+    return cudaGetLastError() == cudaSuccess ? CDFGNN_OK : CDFGNN_ECUDA;
+}
+
+}  // namespace cdfgnn

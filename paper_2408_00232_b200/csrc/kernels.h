@@ -95,6 +95,18 @@ void launch_gemm_simt(bool TA, bool TB, int64_t M, int64_t N, int64_t K, const f
                       int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                       const float* mask, int64_t ldm, float* splitk_ws, int64_t splitk_cap,
                       bool accumulate, cudaStream_t s);
+// tcgen05 TF32 GEMMs (gemm_tc.cu); return a CDFGNN status
+int launch_pad_rows(const float* src, int64_t rows, int64_t cols, float* dst, int64_t ldd, cudaStream_t s);
+int launch_transpose(const float* src, int64_t rows, int64_t cols, int64_t lds, float* dst, int64_t ldd,
+                     cudaStream_t s);
+// split3: 3xTF32 (A_hi·B_hi + A_hi·B_lo + A_lo·B_hi, ~fp32 accuracy); else 1xTF32 (RN inputs)
+int gemm_tc_fwd(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* Bt, int64_t ldb,
+                float* C, int64_t ldc, bool split3, cudaStream_t s);
+int gemm_tc_bwd_data(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* Bk, int64_t ldb,
+                     float* C, int64_t ldc, const float* mask, int64_t ldm, bool split3, cudaStream_t s);
+int gemm_tc_wgrad(int64_t M, int64_t N, int64_t K, const float* Ht, int64_t ldh, const float* St, int64_t lds,
+                  float* C, int64_t ldc, float* ws, int64_t ws_cap, bool accumulate, bool split3,
+                  cudaStream_t s, int* launches);
 void launch_relu(const float* Z, float* H, int64_t count, cudaStream_t s);
 void launch_loss(const float* logits, int64_t ld, int C, int64_t n, int64_t B, int64_t M,
                  const int32_t* labels, const uint8_t* train, double inv_ntrain, float* dlogits,

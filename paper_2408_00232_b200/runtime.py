@@ -21,6 +21,9 @@ def local_inputs(ds, pv: Dict, ld0: int):
         np.ascontiguousarray(ds.train[l2g], dtype=np.uint8)
 
 
+GEMM_MODES = {"fp32": 0, "tf32": 1, "tf32x3": 3}   # cfg.gemm_tf32: SIMT fp32 / tcgen05 1x / 3x TF32
+
+
 class Run:
     """One process's view of a CDFGNN training run (one GPU, k local parts)."""
 
@@ -28,7 +31,8 @@ class Run:
                  cache: bool = True, quant_bits: int = 8, eps0: float = 0.01,
                  adaptive: bool = True, optimizer: str = "adam", lr: float = 0.01,
                  timing: bool = False, plan: Optional[api.Plan] = None,
-                 host_inputs: bool = False, partition_kw: Optional[Dict] = None):
+                 host_inputs: bool = False, partition_kw: Optional[Dict] = None,
+                 gemm: str = "tf32x3"):
         import torch
         self.torch = torch
         self.ds = ds
@@ -40,7 +44,7 @@ class Run:
         self.cfg = api.cfg_default(ds.dims, cache_on=int(cache), quant_bits=quant_bits,
                                    eps_init=eps0, adaptive=int(adaptive),
                                    optimizer=1 if optimizer == "adam" else 0, lr=lr,
-                                   timing=int(timing))
+                                   timing=int(timing), gemm_tf32=GEMM_MODES[gemm])
         nbytes = api.workspace_size(self.plan, self.parts, self.cfg)
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         uid = None
