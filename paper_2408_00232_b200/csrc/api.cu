@@ -76,6 +76,7 @@ struct LocalPart {
     std::vector<int64_t> capA, capB;   // region capacities per peer
     // device
     int32_t *rowptr = nullptr, *colidx = nullptr, *halo_local = nullptr;
+    int32_t* order = nullptr;          // SpMM row order: degree-descending (longest first)
     float* val = nullptr;
     int64_t *moff_d = nullptr, *hoff_d = nullptr;
     uint8_t* regA[kMaxParts] = {};
@@ -210,6 +211,7 @@ void carve(cdfgnn_ctx* c, Bump& b) {
     for (LocalPart& P : c->parts) {
         P.rowptr = b.take<int32_t>(P.n + 1);
         P.colidx = b.take<int32_t>(P.nnz);
+        P.order = b.take<int32_t>(P.n);
         P.val = b.take<float>(P.nnz);
         P.halo_local = b.take<int32_t>(P.hoff[p]);
         P.moff_d = b.take<int64_t>(p + 1);
@@ -495,7 +497,7 @@ int read_stats_now(cdfgnn_ctx* c, int l, int dir, int64_t wire, cudaStream_t s,
 
 int spmm_part(cdfgnn_ctx* c, LocalPart& P, const float* T, float* Y, int64_t ld, cudaStream_t s) {
     mark(c, PH_SPMM, s, ld);
-    launch_spmm(P.rowptr, P.colidx, P.val, P.n, T, Y, ld, s);
+    launch_spmm(P.rowptr, P.colidx, P.val, P.n, T, Y, ld, P.order, s);
     c->launches++;
     return check_launch("spmm");
 }
@@ -659,6 +661,15 @@ extern "C" int cdfgnn_init(const cdfgnn_plan* plan, const int32_t* parts, int32_
         CUDA_TRY(cudaMemcpyAsync(P.rowptr, P.rowptr_h, sizeof(int32_t) * (P.n + 1), cudaMemcpyHostToDevice, s));
         CUDA_TRY(cudaMemcpyAsync(P.colidx, P.colidx_h, sizeof(int32_t) * P.nnz, cudaMemcpyHostToDevice, s));
         CUDA_TRY(cudaMemcpyAsync(P.val, P.val_h, sizeof(float) * P.nnz, cudaMemcpyHostToDevice, s));
+        {
+            std::vector<int32_t> ord(P.n);
+            for (int64_t r = 0; r < P.n; ++r) ord[r] = (int32_t)r;
+            std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+                return (P.rowptr_h[x + 1] - P.rowptr_h[x]) > (P.rowptr_h[y + 1] - P.rowptr_h[y]);
+            });
+            CUDA_TRY(cudaMemcpyAsync(P.order, ord.data(), sizeof(int32_t) * P.n, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+        }
         CUDA_TRY(cudaMemcpyAsync(P.halo_local, P.halo_h, sizeof(int32_t) * P.hoff[c->p], cudaMemcpyHostToDevice, s));
         CUDA_TRY(cudaMemcpyAsync(P.moff_d, P.moff.data(), sizeof(int64_t) * (c->p + 1), cudaMemcpyHostToDevice, s));
         CUDA_TRY(cudaMemcpyAsync(P.hoff_d, P.hoff.data(), sizeof(int64_t) * (c->p + 1), cudaMemcpyHostToDevice, s));
@@ -1006,7 +1017,7 @@ extern "C" int cdfgnn_spmm(cdfgnn_ctx* c, int32_t lp, const float* T, float* Y, 
     if (ld % 4 || ld < F || ld > 1024) CDF_FAIL(CDFGNN_EUSAGE, "ld must be a multiple of 4 in [F, 1024]");
     CUDA_TRY(cudaSetDevice(c->device));
     LocalPart& P = c->parts[lp];
-    launch_spmm(P.rowptr, P.colidx, P.val, P.n, T, Y, ld, (cudaStream_t)stream);
+    launch_spmm(P.rowptr, P.colidx, P.val, P.n, T, Y, ld, P.order, (cudaStream_t)stream);
     return check_launch("spmm");
 }
 

@@ -83,8 +83,9 @@ int launch_scatter_pack_n(const HaloDev& h, const SyncArgs& a, int ntiles, cudaS
 int launch_mirror_apply(const HaloDev& h, const SyncArgs& a, cudaStream_t s);
 
 // ---- SpMM (kernels_spmm.cu): Y[n x ld] = Â T
+// order: row visiting order (degree-descending permutation) or nullptr for identity
 void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val, int64_t n,
-                 const float* T, float* Y, int64_t ld, cudaStream_t s);
+                 const float* T, float* Y, int64_t ld, const int32_t* order, cudaStream_t s);
 
 // ---- dense (kernels_dense.cu)
 // C[M x ldc] = op(A) op(B) (+ mask) ; columns [N, ldc) of C are written as zero.
