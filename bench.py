@@ -37,6 +37,7 @@ def parse():
     ap.add_argument("--mode", default="cache_int8",
                     choices=["cache_int8", "cache_fp32", "quant_only", "nocache"])
     ap.add_argument("--eps0", type=float, default=0.01)
+    ap.add_argument("--transport", default="push", choices=["push", "nccl"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-frac", type=float, default=0.01)
@@ -220,7 +221,7 @@ def main(args):
             "nocache": (False, 0)}[args.mode]
     run = Run(ds, world, rank=rank, world=world, device=local, cache=mode[0], quant_bits=mode[1],
               eps0=args.eps0, adaptive=True, optimizer="adam", lr=0.01, timing=True,
-              host_inputs=not args.no_e2e)
+              host_inputs=not args.no_e2e, transport=args.transport)
     t_prep = time.time() - t_prep
     for _ in range(args.warmup):
         run.epoch()
@@ -265,6 +266,7 @@ def main(args):
     ms_sync = sum(st["ms_sync"] for st in stats) / args.steps
     ms_spmm = sum(st["ms_spmm"] for st in stats) / args.steps
     ms_gemm = sum(st["ms_gemm"] for st in stats) / args.steps
+    sync_sub = [round(sum(st["ms_sync_sub"][i] for st in stats) / args.steps, 3) for i in range(6)]
     tot = allred([comm_alg, comm_wire, remote, base], sumop)
     max_wire = allred([comm_wire], maxop)[0]
     ms_sync_max = allred([ms_sync], maxop)[0]
@@ -316,6 +318,7 @@ def main(args):
         "config": {"workload": f"{cfgc.key} {cfgc.name}: {ds.n} V, {2 * ds.m} CSR nnz, "
                                f"dims {'-'.join(map(str, cfgc.dims))}",
                    "mode": args.mode, "partitions": world, "parallelism": f"vertex-cut p{world}",
+                   "transport": ["none", "nccl", "nvlink-push"][stats[-1]["transport"]],
                    "l2": "inputs larger than L2 (CSR %.2f GB, X %.2f GB)" %
                          (2 * ds.m * 8 / 1e9, ds.X.nbytes / 1e9)},
         "comm_bytes_per_epoch": int(tot[0]), "comm_wire_bytes_per_epoch": int(tot[1]),
@@ -324,7 +327,9 @@ def main(args):
         "nvlink": {"max_wire_bytes_per_gpu": int(max_wire), "sync_ms": round(ms_sync_max, 3),
                    "frac_of_900": round(max_wire / (ms_sync_max * 1e-3) / 1e9 / NVLINK_GBS, 4)
                    if ms_sync_max > 0 and max_wire > 0 else None},
-        "phase_ms": {"gemm": round(ms_gemm, 3), "spmm": round(ms_spmm, 3), "sync": round(ms_sync, 3)},
+        "phase_ms": {"gemm": round(ms_gemm, 3), "spmm": round(ms_spmm, 3), "sync": round(ms_sync, 3),
+                     "sync_split": dict(zip(["gather_pack", "gather_xfer", "master_apply",
+                                             "scatter_pack", "scatter_xfer", "mirror_apply"], sync_sub))},
         "loss": stats[-1]["loss"], "train_acc": stats[-1]["acc"], "eps": stats[-1]["eps_used"],
         "roofline": {"kernel": f"spmm (ld={sp_ld}, the dominant launch group)", "bound": "hbm",
                      "achieved": round(achieved, 1) if achieved else None, "peak": hbm,

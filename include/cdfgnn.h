@@ -145,6 +145,11 @@ typedef struct {
     int32_t gemm_tf32;                  /* 3: tcgen05 3xTF32 GEMMs (default, ~fp32 accuracy);
                                            1: tcgen05 1xTF32; 0: fp32 SIMT GEMMs */
     int32_t timing;                     /* 1: per-phase CUDA-event timing in epoch stats */
+    int32_t transport;                  /* world > 1: 0 = NVLink push (pack kernels store into
+                                           peers' receive regions through CUDA IPC mappings,
+                                           one NCCL barrier per phase, no host round trip;
+                                           falls back to 1 if IPC is unavailable);
+                                           1 = NCCL grouped send/recv after a count exchange */
 } cdfgnn_cfg;
 
 int cdfgnn_cfg_default(cdfgnn_cfg* cfg);
@@ -174,7 +179,8 @@ typedef struct {
     int64_t scatter_msgs;       /* master -> mirror messages */
     int64_t baseline;           /* 2 M: messages without the cache */
     int64_t bytes_alg;          /* (F+12) per int8 message, 4F+4 per fp32 message */
-    int64_t bytes_wire;         /* bytes handed to NCCL / device copies */
+    int64_t bytes_wire;         /* bytes that crossed to another GPU (NCCL payloads or
+                                   NVLink stores); 0 for co-resident partitions */
 } cdfgnn_sync_stats;
 
 /* One gather + scatter synchronisation of layer l (1..L), direction dir
@@ -219,6 +225,9 @@ typedef struct {
     double spmm_bytes;          /* their gather-model bytes */
     double spmm_bytes_compulsory;   /* their compulsory bytes */
     double spmm_ms_sum;         /* their summed CUDA-event time */
+    double ms_sync_sub[6];      /* halo exchange split: gather pack, gather transfer, master apply,
+                                   scatter pack, scatter transfer, mirror apply */
+    int32_t transport;          /* 0 co-resident, 1 NCCL send/recv, 2 NVLink push */
 } cdfgnn_epoch_stats;
 
 /* Alg. 1 once.  X[k] device (n_i x ld(F_0)), labels[k] int32 [n_i],

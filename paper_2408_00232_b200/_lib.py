@@ -67,7 +67,7 @@ class CfgC(ctypes.Structure):
                 ("nu1", c_f64), ("nu2", c_f64), ("xi", c_f64), ("lam1", c_f64), ("lam2", c_f64),
                 ("eps_clamp", c_i32), ("quant_bits", c_i32), ("optimizer", c_i32), ("lr", c_f64),
                 ("beta1", c_f64), ("beta2", c_f64), ("adam_eps", c_f64), ("gemm_tf32", c_i32),
-                ("timing", c_i32)]
+                ("timing", c_i32), ("transport", c_i32)]
 
 
 class SyncStatsC(ctypes.Structure):
@@ -82,7 +82,8 @@ class EpochStatsC(ctypes.Structure):
                 ("bwd", SyncStatsC * MAX_LAYERS), ("gpu_launches", c_i32), ("ms_gemm", c_f64),
                 ("ms_spmm", c_f64), ("ms_sync", c_f64), ("ms_other", c_f64),
                 ("spmm_ld", c_i32), ("spmm_launches", c_i32), ("spmm_bytes", c_f64),
-                ("spmm_bytes_compulsory", c_f64), ("spmm_ms_sum", c_f64)]
+                ("spmm_bytes_compulsory", c_f64), ("spmm_ms_sum", c_f64),
+                ("ms_sync_sub", c_f64 * 6), ("transport", c_i32)]
 
 
 def _sig(name, res, args):

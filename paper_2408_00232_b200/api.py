@@ -218,7 +218,8 @@ def layer_bwd(ctx: Ctx, l: int, dZ: List, ld: int, H_in: List, ld_in: int, W, dZ
 
 
 def _epoch_dict(s: L.EpochStatsC, nl: int) -> Dict:
-    d = {k: getattr(s, k) for k, _ in L.EpochStatsC._fields_ if k not in ("fwd", "bwd")}
+    d = {k: getattr(s, k) for k, _ in L.EpochStatsC._fields_ if k not in ("fwd", "bwd", "ms_sync_sub")}
+    d["ms_sync_sub"] = list(s.ms_sync_sub)
     d["fwd"] = [_stats_dict(s.fwd[i]) for i in range(nl)]
     d["bwd"] = [_stats_dict(s.bwd[i]) for i in range(nl)]
     return d

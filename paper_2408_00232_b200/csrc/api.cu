@@ -6,6 +6,7 @@
 // (world == p) exchanges message counts and then payloads with grouped NCCL
 // send/recv over NVLink (§3.2 gather / scatter), and sums weight
 // gradients with ncclAllReduce (the "parameter server" of P:L221-222, reading R9).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -64,6 +65,8 @@ struct Bump {
 };
 
 enum Phase { PH_GEMM = 0, PH_SPMM = 1, PH_SYNC = 2, PH_OTHER = 3, PH_END = 4 };
+// sub-phases of the halo exchange (tag of PH_SYNC marks)
+enum SyncSub { SS_GPACK = 0, SS_GXFER = 1, SS_MASTER = 2, SS_SPACK = 3, SS_SXFER = 4, SS_MIRROR = 5 };
 
 struct LocalPart {
     int32_t part = 0;
@@ -135,6 +138,8 @@ struct cdfgnn_ctx {
     size_t ev_used = 0;
     size_t ws_bytes = 0;
     void* ws = nullptr;
+    int transport = 0;                 // 0 co-resident (world 1), 1 NCCL send/recv, 2 NVLink push
+    std::vector<void*> peer_maps;      // IPC-opened peer allocations (push transport)
 };
 
 namespace {
@@ -341,7 +346,7 @@ void build_tables(cdfgnn_ctx* c) {
         h.quant = c->cfg.quant_bits; h.hdr_bytes = c->hdr_bytes;
         h.moff = P.moff_d; h.hoff = P.hoff_d; h.halo_local = P.halo_local;
         h.gsend = P.gsend_d; h.grecv = P.grecv_d; h.ssend = P.ssend_d; h.srecv = P.srecv_d;
-        h.cnt_gsend = P.cnt; h.cnt_ssend = P.cnt + 2 * p;
+        h.remote = 0;
         h.gflag = P.gflag; h.fired = P.fired; h.active = P.active;
         h.idxmap = P.idxmap; h.mmap = P.mmap;
         h.stage_codes = P.stage_codes; h.stage_lohi = P.stage_lohi; h.stage_a = P.stage_a;
@@ -411,12 +416,97 @@ int nccl_phase(cdfgnn_ctx* c, LocalPart& P, bool gather, int64_t rowb, cudaStrea
     return CDFGNN_OK;
 }
 
+// NVLink push: every rank's pack kernels have stored into the peers' receive regions once
+// this stream-ordered all-reduce completes on all ranks (no host round trip)
+int push_barrier(cdfgnn_ctx* c, cudaStream_t s) {
+    NCCL_TRY(ncclAllReduce(c->scal_d + 4, c->scal_d + 4, 1, ncclInt32, ncclSum, c->comm, s));
+    return CDFGNN_OK;
+}
+
+struct PeerInfo {
+    cudaIpcMemHandle_t handle;
+    uint64_t ws_off;                   // workspace offset inside the IPC allocation
+    uint64_t cnt_off;                  // counts array, relative to the workspace
+    uint64_t regA_off[kMaxParts];      // mirror-role regions (receive scatter from master j)
+    uint64_t regB_off[kMaxParts];      // master-role regions (receive gather from source s)
+};
+
+typedef CUresult (*GetRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+// Map every peer's receive regions into this process (CUDA IPC over NVLink) and point
+// the send tables at them.  Returns non-OK (caller falls back to NCCL) if IPC fails.
+int setup_push(cdfgnn_ctx* c, cudaStream_t s) {
+    void* fnp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fnp, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+        CDF_FAIL(CDFGNN_ECUDA, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t sz = 0;
+    if (reinterpret_cast<GetRangeFn>(fnp)(&base, &sz, (CUdeviceptr)c->ws) != CUDA_SUCCESS)
+        CDF_FAIL(CDFGNN_ECUDA, "cuMemGetAddressRange failed");
+    LocalPart& P = c->parts[0];
+    const int p = c->p, me = P.part;
+    PeerInfo mine;
+    std::memset(&mine, 0, sizeof(mine));
+    if (cudaIpcGetMemHandle(&mine.handle, (void*)base) != cudaSuccess) {
+        cudaGetLastError();
+        CDF_FAIL(CDFGNN_ECUDA, "cudaIpcGetMemHandle failed (workspace not IPC-shareable)");
+    }
+    const uint8_t* ws = reinterpret_cast<const uint8_t*>(c->ws);
+    mine.ws_off = (uint64_t)(ws - reinterpret_cast<const uint8_t*>(base));
+    mine.cnt_off = (uint64_t)(reinterpret_cast<const uint8_t*>(P.cnt) - ws);
+    for (int j = 0; j < p; ++j) {
+        mine.regA_off[j] = (uint64_t)(P.regA[j] - ws);
+        mine.regB_off[j] = (uint64_t)(P.regB[j] - ws);
+    }
+    // all-gather the tables through NCCL (device staging in the split-K scratch)
+    uint8_t* dsend = reinterpret_cast<uint8_t*>(c->splitk);
+    uint8_t* drecv = dsend + align_up(sizeof(PeerInfo), 256);
+    if ((int64_t)(align_up(sizeof(PeerInfo), 256) + sizeof(PeerInfo) * p) > c->splitk_cap * 4)
+        CDF_FAIL(CDFGNN_EUSAGE, "scratch too small for the peer table");
+    std::vector<PeerInfo> all(p);
+    CUDA_TRY(cudaMemcpyAsync(dsend, &mine, sizeof(mine), cudaMemcpyHostToDevice, s));
+    NCCL_TRY(ncclAllGather(dsend, drecv, sizeof(PeerInfo), ncclUint8, c->comm, s));
+    CUDA_TRY(cudaMemcpyAsync(all.data(), drecv, sizeof(PeerInfo) * p, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int r = 0; r < p; ++r) {
+        if (r == me) continue;
+        void* mapped = nullptr;
+        if (cudaIpcOpenMemHandle(&mapped, all[r].handle, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            for (void* m : c->peer_maps) cudaIpcCloseMemHandle(m);
+            c->peer_maps.clear();
+            CDF_FAIL(CDFGNN_ECUDA, "cudaIpcOpenMemHandle failed for peer %d", r);
+        }
+        c->peer_maps.push_back(mapped);
+        uint8_t* pws = reinterpret_cast<uint8_t*>(mapped) + all[r].ws_off;
+        int32_t* pcnt = reinterpret_cast<int32_t*>(pws + all[r].cnt_off);
+        // gather: my mirror slab for master r -> r's master-role region for source me
+        P.gsend_h.hdr[r] = pws + all[r].regB_off[me];
+        P.gsend_h.pay[r] = P.gsend_h.hdr[r] + align_up(P.capA[r] * c->hdr_bytes, 256);
+        P.gsend_h.cnt[r] = pcnt + p + me;
+        // scatter: my halo list for mirror part r -> r's mirror-role region for master me
+        P.ssend_h.hdr[r] = pws + all[r].regA_off[me];
+        P.ssend_h.pay[r] = P.ssend_h.hdr[r] + align_up(P.capB[r] * c->hdr_bytes, 256);
+        P.ssend_h.cnt[r] = pcnt + 3 * p + me;
+    }
+    CUDA_TRY(cudaMemcpyAsync(P.gsend_d, &P.gsend_h, sizeof(RegionTab), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(P.ssend_d, &P.ssend_h, sizeof(RegionTab), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    P.halo.remote = 1;
+    // every rank must have mapped its peers before anyone pushes
+    NCCL_TRY(ncclAllReduce(c->scal_d + 4, c->scal_d + 4, 1, ncclInt32, ncclSum, c->comm, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return CDFGNN_OK;
+}
+
 int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float eps,
               cudaStream_t s, int64_t* wire) {
     const int p = c->p;
     const int F = (int)sync_width(c, l);
     if (ld != ld_of(F)) CDF_FAIL(CDFGNN_EUSAGE, "ld %lld must equal roundup(F=%d, 4)", (long long)ld, F);
-    mark(c, PH_SYNC, s);
+    mark(c, PH_SYNC, s, SS_GPACK);
     std::vector<SyncArgs> args(c->k);
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
@@ -431,14 +521,16 @@ int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float 
     // ---- gather: mirrors test, quantise, pack (Alg. 2 L3-L9)
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
-        CUDA_TRY(cudaMemsetAsync(P.cnt, 0, sizeof(int32_t) * p, s));
         const int nt = gather_tiles_host(P.moff.data(), p, ld);
         args[t].ticket_base_g = P.tbase_g;
         c->launches += launch_gather_pack_n(P.halo, args[t], nt, s);
         P.tbase_g += nt;
     }
     CDF_TRY(check_launch("gather_pack"));
-    if (c->world > 1) CDF_TRY(nccl_phase(c, c->parts[0], true, rowb, s, wire));
+    mark(c, PH_SYNC, s, SS_GXFER);
+    if (c->transport == 1) CDF_TRY(nccl_phase(c, c->parts[0], true, rowb, s, wire));
+    if (c->transport == 2) CDF_TRY(push_barrier(c, s));
+    mark(c, PH_SYNC, s, SS_MASTER);
     // ---- masters: apply in ascending source order, own test, stage scatter (L10-L19)
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
@@ -448,17 +540,20 @@ int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float 
         c->launches += launch_master(P.halo, args[t], s);
     }
     CDF_TRY(check_launch("master"));
+    mark(c, PH_SYNC, s, SS_SPACK);
     // ---- scatter: active masters to every mirror (L20-L22)
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
-        CUDA_TRY(cudaMemsetAsync(P.cnt + 2 * p, 0, sizeof(int32_t) * p, s));
         const int nt = scatter_tiles_host(P.hoff.data(), p);
         args[t].ticket_base_s = P.tbase_s;
         c->launches += launch_scatter_pack_n(P.halo, args[t], nt, s);
         P.tbase_s += nt;
     }
     CDF_TRY(check_launch("scatter_pack"));
-    if (c->world > 1) CDF_TRY(nccl_phase(c, c->parts[0], false, rowb, s, wire));
+    mark(c, PH_SYNC, s, SS_SXFER);
+    if (c->transport == 1) CDF_TRY(nccl_phase(c, c->parts[0], false, rowb, s, wire));
+    if (c->transport == 2) CDF_TRY(push_barrier(c, s));
+    mark(c, PH_SYNC, s, SS_MIRROR);
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
         if (P.M == 0) continue;
@@ -483,6 +578,8 @@ void fill_sync_stats(const cdfgnn_ctx* c, int l, int dir, const unsigned long lo
     const int64_t mb = c->cfg.quant_bits ? F + 12 : 4 * F + 4;
     st->bytes_alg = (h[0] + h[3]) * mb;
     st->bytes_wire = wire;
+    if (c->transport == 2)      // NVLink push: every message is stored into a peer GPU
+        st->bytes_wire = (int64_t)(h[0] + h[3]) * (c->hdr_bytes + (c->cfg.quant_bits ? F : 4 * ld_of(F)));
     (void)dir;
 }
 
@@ -682,10 +779,32 @@ extern "C" int cdfgnn_init(const cdfgnn_plan* plan, const int32_t* parts, int32_
     CUDA_TRY(cudaMallocHost(&c->stats_h, sizeof(long long) * CDFGNN_MAX_LAYERS * 2 * 4));
     CUDA_TRY(cudaMallocHost(&c->host_scratch, sizeof(double) * (c->k + 8)));
     CUDA_TRY(cudaStreamSynchronize(s));
+    c->transport = 0;
     if (world > 1) {
         ncclUniqueId id;
         std::memcpy(&id, nccl_uid, sizeof(id));
         NCCL_TRY(ncclCommInitRank(&c->comm, world, id, rank));
+        c->transport = 1;
+        if (cfg->transport == 0) {
+            // all ranks must agree: push only if every rank mapped its peers
+            int ok = setup_push(c.get(), s) == CDFGNN_OK ? 1 : 0;
+            int32_t* flag = c->scal_d + 5;
+            CUDA_TRY(cudaMemcpyAsync(flag, &ok, sizeof(int), cudaMemcpyHostToDevice, s));
+            NCCL_TRY(ncclAllReduce(flag, flag, 1, ncclInt32, ncclMin, c->comm, s));
+            CUDA_TRY(cudaMemcpyAsync(&ok, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            if (ok) {
+                c->transport = 2;
+            } else {
+                // restore the NCCL send tables
+                build_tables(c.get());
+                LocalPart& P = c->parts[0];
+                CUDA_TRY(cudaMemcpy(P.gsend_d, &P.gsend_h, sizeof(RegionTab), cudaMemcpyHostToDevice));
+                CUDA_TRY(cudaMemcpy(P.ssend_d, &P.ssend_h, sizeof(RegionTab), cudaMemcpyHostToDevice));
+                for (void* m : c->peer_maps) cudaIpcCloseMemHandle(m);
+                c->peer_maps.clear();
+            }
+        }
     }
     c->eps = cfg->eps_init;
     c->timing = cfg->timing != 0;
@@ -695,6 +814,8 @@ extern "C" int cdfgnn_init(const cdfgnn_plan* plan, const int32_t* parts, int32_
 
 extern "C" int cdfgnn_destroy(cdfgnn_ctx* c) {
     if (!c) return CDFGNN_OK;
+    if (!c->peer_maps.empty()) cudaDeviceSynchronize();
+    for (void* m : c->peer_maps) cudaIpcCloseMemHandle(m);
     if (c->comm) ncclCommDestroy(c->comm);
     for (LocalPart& P : c->parts)
         if (P.cnt_h) cudaFreeHost(P.cnt_h);
@@ -864,6 +985,7 @@ static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const
                 fill_sync_stats(c, l, dir, c->stats_h + ((l - 1) * 2 + dir) * 4, wire[l - 1][dir],
                                 dir ? &out->bwd[l - 1] : &out->fwd[l - 1]);
         out->gpu_launches = c->launches;
+        out->transport = c->transport;
         if (c->timing && c->ev_used >= 2) {
             double ph[5] = {0, 0, 0, 0, 0};
             std::vector<std::pair<int64_t, std::pair<int, double>>> per;   // ld -> (launches, ms)
@@ -871,6 +993,8 @@ static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const
                 float ms = 0.f;
                 cudaEventElapsedTime(&ms, c->ev[e], c->ev[e + 1]);
                 ph[c->ev_phase[e]] += ms;
+                if (c->ev_phase[e] == PH_SYNC && c->ev_tag[e] >= 0 && c->ev_tag[e] < 6)
+                    out->ms_sync_sub[c->ev_tag[e]] += ms;
                 if (c->ev_phase[e] == PH_SPMM) {
                     bool found = false;
                     for (auto& q : per)

@@ -18,7 +18,7 @@ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 struct RegionTab {
     uint8_t* hdr[kMaxParts];
     uint8_t* pay[kMaxParts];
-    const int32_t* cnt[kMaxParts];   // message count of the region (receive tables)
+    int32_t* cnt[kMaxParts];   // message count slot of the region (written by the sender)
 };
 
 // Everything the halo kernels need about one local part (device pointers).
@@ -34,8 +34,7 @@ struct HaloDev {
     const RegionTab* grecv;    // gather messages received, per source part
     const RegionTab* ssend;    // master-role send regions (scatter), per mirror peer
     const RegionTab* srecv;    // scatter messages received, per master part
-    int32_t* cnt_gsend;        // [p]
-    int32_t* cnt_ssend;        // [p]
+    int remote;                // send regions live in peer GPUs' memory (NVLink push)
     uint8_t* gflag;            // [M]
     uint8_t* fired;            // [B]
     uint8_t* active;           // [B]

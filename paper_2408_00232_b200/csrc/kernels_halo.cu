@@ -69,26 +69,43 @@ __device__ __forceinline__ void setc(float4& v, int k, float x) {
 __device__ __forceinline__ unsigned long long mkstat(uint32_t seq, uint32_t kind, uint32_t v) {
     return ((unsigned long long)seq << 32) | ((unsigned long long)kind << 30) | (v & 0x3FFFFFFFu);
 }
-// called by one thread; returns the exclusive prefix of `tile` within its segment
-__device__ uint32_t lookback(unsigned long long* status, int tile, bool first_in_seg,
-                             uint32_t count, uint32_t seq) {
-    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(status[tile]);
-    if (first_in_seg) {
-        me.store(mkstat(seq, 2, count), cuda::memory_order_release);
-        return 0;
+// Called by a whole warp; returns (to every lane) the exclusive prefix of `tile` within its
+// segment.  Lanes inspect 32 predecessors per round (decoupled look-back): the window's
+// aggregates are summed up to the closest inclusive prefix.  Tiles are numbered by a
+// ticket taken when the block starts, so every predecessor is running or done.
+__device__ uint32_t lookback_warp(unsigned long long* status, int tile, bool first_in_seg,
+                                  uint32_t count, uint32_t seq, int lane) {
+    if (lane == 0) {
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(status[tile]);
+        me.store(mkstat(seq, first_in_seg ? 2u : 1u, count), cuda::memory_order_release);
     }
-    me.store(mkstat(seq, 1, count), cuda::memory_order_release);
+    if (first_in_seg) return 0;
     uint32_t excl = 0;
-    for (int j = tile - 1;; --j) {
-        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[j]);
-        unsigned long long w;
-        do {
-            w = st.load(cuda::memory_order_acquire);
-        } while ((uint32_t)(w >> 32) != seq || ((w >> 30) & 3u) == 0u);
-        excl += (uint32_t)(w & 0x3FFFFFFFu);
-        if (((w >> 30) & 3u) == 2u) break;
+    int j = tile - 1;
+    while (true) {
+        const int idx = j - lane;
+        unsigned long long w = mkstat(seq, 2, 0);            // below tile 0: empty prefix
+        if (idx >= 0) {
+            cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[idx]);
+            bool ready;
+            do {
+                w = st.load(cuda::memory_order_acquire);
+                ready = (uint32_t)(w >> 32) == seq && ((w >> 30) & 3u) != 0u;
+            } while (!ready);
+        }
+        const unsigned isp = __ballot_sync(0xffffffffu, ((w >> 30) & 3u) == 2u);
+        const int stop = isp ? __ffs(isp) - 1 : 31;           // closest inclusive prefix
+        uint32_t v = lane <= stop ? (uint32_t)(w & 0x3FFFFFFFu) : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (isp) break;
+        j -= 32;
     }
-    me.store(mkstat(seq, 2, excl + count), cuda::memory_order_release);
+    if (lane == 0) {
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(status[tile]);
+        me.store(mkstat(seq, 2, excl + count), cuda::memory_order_release);
+    }
     return excl;
 }
 
@@ -162,15 +179,18 @@ __global__ void __launch_bounds__(kThreads) gather_pack_kernel(HaloDev h, SyncAr
     const unsigned bal = __ballot_sync(0xffffffffu, flag && gl == 0);
     if (lane == 0) s_wcnt[warp] = __popc(bal);
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
         uint32_t cnt = 0;
         for (int w = 0; w < kWarps; ++w) cnt += s_wcnt[w];
         const int ntiles_seg = (int)((seg_len + TR - 1) / TR);
-        const uint32_t excl = lookback(h.status_g, tile, ltile == 0, cnt, a.seq);
-        s_excl = excl;
-        if (ltile == ntiles_seg - 1) {
-            h.cnt_gsend[seg] = (int32_t)(excl + cnt);
-            atomicAdd(&a.stats[0], (unsigned long long)(excl + cnt));
+        const uint32_t excl = lookback_warp(h.status_g, tile, ltile == 0, cnt, a.seq, lane);
+        if (lane == 0) {
+            s_excl = excl;
+            if (ltile == ntiles_seg - 1) {
+                *h.gsend->cnt[seg] = (int32_t)(excl + cnt);
+                if (h.remote) __threadfence_system();
+                atomicAdd(&a.stats[0], (unsigned long long)(excl + cnt));
+            }
         }
     }
     __syncthreads();
@@ -226,6 +246,7 @@ __global__ void __launch_bounds__(kThreads) gather_pack_kernel(HaloDev h, SyncAr
             if (sr) st4(sr + c0, x[v]);   // Alg. 2 L6: s ← z
         }
     }
+    if (h.remote) __threadfence_system();   // pushed to a peer GPU: visible before the barrier
 }
 
 // ==================================================================================
@@ -453,15 +474,18 @@ __global__ void __launch_bounds__(kThreads) scatter_pack_kernel(HaloDev h, SyncA
     const unsigned bal = __ballot_sync(0xffffffffu, flag);
     if (lane == 0) s_wcnt[warp] = __popc(bal);
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
         uint32_t cnt = 0;
         for (int w = 0; w < kWarps; ++w) cnt += s_wcnt[w];
         const int ntiles_seg = (int)((seg_len + kScatterTile - 1) / kScatterTile);
-        const uint32_t excl = lookback(h.status_s, tile, ltile == 0, cnt, a.seq);
-        s_excl = excl;
-        if (ltile == ntiles_seg - 1) {
-            h.cnt_ssend[seg] = (int32_t)(excl + cnt);
-            atomicAdd(&a.stats[3], (unsigned long long)(excl + cnt));
+        const uint32_t excl = lookback_warp(h.status_s, tile, ltile == 0, cnt, a.seq, lane);
+        if (lane == 0) {
+            s_excl = excl;
+            if (ltile == ntiles_seg - 1) {
+                *h.ssend->cnt[seg] = (int32_t)(excl + cnt);
+                if (h.remote) __threadfence_system();
+                atomicAdd(&a.stats[3], (unsigned long long)(excl + cnt));
+            }
         }
     }
     int woff = 0;
@@ -494,6 +518,7 @@ __global__ void __launch_bounds__(kThreads) scatter_pack_kernel(HaloDev h, SyncA
             for (int c = lane * 4; c < a.ld; c += 128) st4(dst + c, ld4(src + c));
         }
     }
+    if (h.remote) __threadfence_system();
 }
 
 // ==================================================================================

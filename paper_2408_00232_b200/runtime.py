@@ -32,7 +32,7 @@ class Run:
                  adaptive: bool = True, optimizer: str = "adam", lr: float = 0.01,
                  timing: bool = False, plan: Optional[api.Plan] = None,
                  host_inputs: bool = False, partition_kw: Optional[Dict] = None,
-                 gemm: str = "tf32x3"):
+                 gemm: str = "tf32x3", transport: str = "push"):
         import torch
         self.torch = torch
         self.ds = ds
@@ -44,7 +44,8 @@ class Run:
         self.cfg = api.cfg_default(ds.dims, cache_on=int(cache), quant_bits=quant_bits,
                                    eps_init=eps0, adaptive=int(adaptive),
                                    optimizer=1 if optimizer == "adam" else 0, lr=lr,
-                                   timing=int(timing), gemm_tf32=GEMM_MODES[gemm])
+                                   timing=int(timing), gemm_tf32=GEMM_MODES[gemm],
+                                   transport={"push": 0, "nccl": 1}[transport])
         nbytes = api.workspace_size(self.plan, self.parts, self.cfg)
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         uid = None

@@ -15,14 +15,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("mode", ["exact", "cache_int8"])
-def test_two_gpus_match_one_gpu(mode):
+@pytest.mark.parametrize("transport", ["push", "nccl"])
+def test_two_gpus_match_one_gpu(mode, transport):
     torch = require_gpu()
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
            "--master-addr", "127.0.0.1", "--master-port", "29517",
-           os.path.join(ROOT, "tools", "mgpu_check.py"), "--mode", mode, "--epochs", "4"]
+           os.path.join(ROOT, "tools", "mgpu_check.py"), "--mode", mode, "--epochs", "4",
+           "--transport", transport]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
