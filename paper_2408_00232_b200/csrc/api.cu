@@ -86,6 +86,7 @@ struct LocalPart {
     uint8_t* regB[kMaxParts] = {};
     RegionTab *gsend_d = nullptr, *grecv_d = nullptr, *ssend_d = nullptr, *srecv_d = nullptr;
     RegionTab gsend_h{}, grecv_h{}, ssend_h{}, srecv_h{};
+    PutTab *putG_d = nullptr, *putS_d = nullptr;   // NVLink push of gather / scatter messages
     int32_t* cnt = nullptr;           // [4p]: gsend | grecv | ssend | srecv
     int32_t* cnt_h = nullptr;         // pinned
     uint8_t *gflag = nullptr, *fired = nullptr, *active = nullptr;
@@ -229,6 +230,8 @@ void carve(cdfgnn_ctx* c, Bump& b) {
         P.grecv_d = b.take<RegionTab>(1);
         P.ssend_d = b.take<RegionTab>(1);
         P.srecv_d = b.take<RegionTab>(1);
+        P.putG_d = b.take<PutTab>(1);
+        P.putS_d = b.take<PutTab>(1);
         P.cnt = b.take<int32_t>(4 * p);
         P.gflag = b.take<uint8_t>(P.M);
         P.fired = b.take<uint8_t>(P.B);
@@ -470,6 +473,9 @@ int setup_push(cdfgnn_ctx* c, cudaStream_t s) {
     NCCL_TRY(ncclAllGather(dsend, drecv, sizeof(PeerInfo), ncclUint8, c->comm, s));
     CUDA_TRY(cudaMemcpyAsync(all.data(), drecv, sizeof(PeerInfo) * p, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    PutTab pg, ps;
+    std::memset(&pg, 0, sizeof(pg));
+    std::memset(&ps, 0, sizeof(ps));
     for (int r = 0; r < p; ++r) {
         if (r == me) continue;
         void* mapped = nullptr;
@@ -482,19 +488,24 @@ int setup_push(cdfgnn_ctx* c, cudaStream_t s) {
         c->peer_maps.push_back(mapped);
         uint8_t* pws = reinterpret_cast<uint8_t*>(mapped) + all[r].ws_off;
         int32_t* pcnt = reinterpret_cast<int32_t*>(pws + all[r].cnt_off);
-        // gather: my mirror slab for master r -> r's master-role region for source me
-        P.gsend_h.hdr[r] = pws + all[r].regB_off[me];
-        P.gsend_h.pay[r] = P.gsend_h.hdr[r] + align_up(P.capA[r] * c->hdr_bytes, 256);
-        P.gsend_h.cnt[r] = pcnt + p + me;
-        // scatter: my halo list for mirror part r -> r's mirror-role region for master me
-        P.ssend_h.hdr[r] = pws + all[r].regA_off[me];
-        P.ssend_h.pay[r] = P.ssend_h.hdr[r] + align_up(P.capB[r] * c->hdr_bytes, 256);
-        P.ssend_h.cnt[r] = pcnt + 3 * p + me;
+        // gather: my packed mirror slab for master r -> r's master-role region for source me
+        pg.src_hdr[r] = P.gsend_h.hdr[r];
+        pg.src_pay[r] = P.gsend_h.pay[r];
+        pg.src_cnt[r] = P.gsend_h.cnt[r];
+        pg.dst_hdr[r] = pws + all[r].regB_off[me];
+        pg.dst_pay[r] = pg.dst_hdr[r] + align_up(P.capA[r] * c->hdr_bytes, 256);
+        pg.dst_cnt[r] = pcnt + p + me;
+        // scatter: my packed halo list for mirror part r -> r's mirror-role region for master me
+        ps.src_hdr[r] = P.ssend_h.hdr[r];
+        ps.src_pay[r] = P.ssend_h.pay[r];
+        ps.src_cnt[r] = P.ssend_h.cnt[r];
+        ps.dst_hdr[r] = pws + all[r].regA_off[me];
+        ps.dst_pay[r] = ps.dst_hdr[r] + align_up(P.capB[r] * c->hdr_bytes, 256);
+        ps.dst_cnt[r] = pcnt + 3 * p + me;
     }
-    CUDA_TRY(cudaMemcpyAsync(P.gsend_d, &P.gsend_h, sizeof(RegionTab), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(P.ssend_d, &P.ssend_h, sizeof(RegionTab), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(P.putG_d, &pg, sizeof(PutTab), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(P.putS_d, &ps, sizeof(PutTab), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaStreamSynchronize(s));
-    P.halo.remote = 1;
     // every rank must have mapped its peers before anyone pushes
     NCCL_TRY(ncclAllReduce(c->scal_d + 4, c->scal_d + 4, 1, ncclInt32, ncclSum, c->comm, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -529,7 +540,13 @@ int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float 
     CDF_TRY(check_launch("gather_pack"));
     mark(c, PH_SYNC, s, SS_GXFER);
     if (c->transport == 1) CDF_TRY(nccl_phase(c, c->parts[0], true, rowb, s, wire));
-    if (c->transport == 2) CDF_TRY(push_barrier(c, s));
+    if (c->transport == 2) {
+        LocalPart& P = c->parts[0];
+        c->launches += launch_put(P.putG_d, p, c->hdr_bytes, rowb,
+                                  *std::max_element(P.capA.begin(), P.capA.end()), s);
+        CDF_TRY(check_launch("put gather"));
+        CDF_TRY(push_barrier(c, s));
+    }
     mark(c, PH_SYNC, s, SS_MASTER);
     // ---- masters: apply in ascending source order, own test, stage scatter (L10-L19)
     for (int t = 0; t < c->k; ++t) {
@@ -552,7 +569,13 @@ int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float 
     CDF_TRY(check_launch("scatter_pack"));
     mark(c, PH_SYNC, s, SS_SXFER);
     if (c->transport == 1) CDF_TRY(nccl_phase(c, c->parts[0], false, rowb, s, wire));
-    if (c->transport == 2) CDF_TRY(push_barrier(c, s));
+    if (c->transport == 2) {
+        LocalPart& P = c->parts[0];
+        c->launches += launch_put(P.putS_d, p, c->hdr_bytes, rowb,
+                                  *std::max_element(P.capB.begin(), P.capB.end()), s);
+        CDF_TRY(check_launch("put scatter"));
+        CDF_TRY(push_barrier(c, s));
+    }
     mark(c, PH_SYNC, s, SS_MIRROR);
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];

@@ -49,6 +49,19 @@ struct HaloDev {
     int32_t* err;              // protocol error flag (device)
 };
 
+// NVLink put: copy each peer's compacted messages (count from device memory) from local
+// staging into the peer GPU's receive region through a CUDA-IPC mapping.
+struct PutTab {
+    const uint8_t* src_hdr[kMaxParts];
+    const uint8_t* src_pay[kMaxParts];
+    const int32_t* src_cnt[kMaxParts];
+    uint8_t* dst_hdr[kMaxParts];      // nullptr: no peer
+    uint8_t* dst_pay[kMaxParts];
+    int32_t* dst_cnt[kMaxParts];
+};
+int launch_put(const PutTab* tab, int p, int64_t hdr_bytes, int64_t row_bytes, int64_t max_count,
+               cudaStream_t s);
+
 // Cache tables of one (layer, direction) of one part (may be null with cache off).
 struct CacheDev {
     float* s_mir;   // [M*ld]

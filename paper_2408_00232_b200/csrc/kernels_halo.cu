@@ -16,6 +16,8 @@
 // reading R15, so masks and codes are bit-identical to oracle/cache.py's fp32 replay.
 #include <cuda/atomic>
 
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace cdfgnn {
@@ -116,12 +118,15 @@ __device__ __forceinline__ int find_seg(const int64_t* off, int p, int64_t idx) 
 }
 
 // ==================================================================================
-// gather_pack: one tile = 8 warps x (32/LPR) mirror rows, all within one master peer
+// gather_pack: one tile = 8 warps x RPW x (32/LPR) mirror rows, all within one master
+// peer.  Each warp tests RPW row groups back to back (loads of all of them in flight),
+// the tile's senders are ranked in row order and the tile's offset inside its peer's
+// message buffer comes from the decoupled look-back, so the buffer keeps halo-list order.
 // ==================================================================================
-template <int LPR, int VPL>
+template <int LPR, int VPL, int RPW>
 __global__ void __launch_bounds__(kThreads) gather_pack_kernel(HaloDev h, SyncArgs a) {
     constexpr int GPW = 32 / LPR;
-    constexpr int TR = kWarps * GPW;
+    constexpr int TR = kWarps * GPW * RPW;
     __shared__ int s_tile;
     __shared__ int s_wcnt[kWarps];
     __shared__ uint32_t s_excl;
@@ -143,41 +148,53 @@ __global__ void __launch_bounds__(kThreads) gather_pack_kernel(HaloDev h, SyncAr
     const int ltile = tile - tbase;
     const int64_t seg_len = s_moff[seg + 1] - s_moff[seg];
     const int g = lane / LPR, gl = lane % LPR;
-    const int64_t ridx = (int64_t)ltile * TR + warp * GPW + g;      // position in halo list
-    const bool valid = ridx < seg_len;
-    const int64_t mrow = s_moff[seg] + (valid ? ridx : 0);          // mirror index
-    const float* xr = a.X + (h.B + mrow) * a.ld;
-    float* sr = a.nocache ? nullptr : a.c.s_mir + mrow * a.ld;
-    float4 d[VPL], x[VPL];
-    float maxd = 0.f, maxs = 0.f, lo = INFINITY, hi = -INFINITY;
+    float4 d[RPW][VPL];
+    float lo[RPW], hi[RPW];
+    bool flag[RPW];
+    unsigned bal[RPW];
+    int64_t ridx[RPW];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-        const int c0 = (gl + v * LPR) * 4;
-        x[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid && c0 < a.ld) {
-            x[v] = ld4(xr + c0);
-            if (sr) s4 = ld4(sr + c0);
-        }
+    for (int r = 0; r < RPW; ++r) {
+        ridx[r] = (int64_t)ltile * TR + (warp * RPW + r) * GPW + g;   // position in halo list
+        const bool valid = ridx[r] < seg_len;
+        const int64_t mrow = s_moff[seg] + (valid ? ridx[r] : 0);     // mirror index
+        const float* xr = a.X + (h.B + mrow) * a.ld;
+        const float* sr = a.nocache ? nullptr : a.c.s_mir + mrow * a.ld;
+        float maxd = 0.f, maxs = 0.f;
+        lo[r] = INFINITY;
+        hi[r] = -INFINITY;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float dk = __fsub_rn(comp(x[v], k), comp(s4, k));
-            setc(d[v], k, dk);
-            if (c0 + k < a.F) {
-                maxd = fmaxf(maxd, fabsf(dk));
-                maxs = fmaxf(maxs, fabsf(comp(s4, k)));
-                lo = fminf(lo, dk);
-                hi = fmaxf(hi, dk);
+        for (int v = 0; v < VPL; ++v) {
+            const int c0 = (gl + v * LPR) * 4;
+            float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f), s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (valid && c0 < a.ld) {
+                x4 = ld4(xr + c0);
+                if (sr) s4 = ld4(sr + c0);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float dk = __fsub_rn(comp(x4, k), comp(s4, k));
+                setc(d[r][v], k, dk);
+                if (c0 + k < a.F) {
+                    maxd = fmaxf(maxd, fabsf(dk));
+                    maxs = fmaxf(maxs, fabsf(comp(s4, k)));
+                    lo[r] = fminf(lo[r], dk);
+                    hi[r] = fmaxf(hi[r], dk);
+                }
             }
         }
+        maxd = gmax<LPR>(maxd);
+        maxs = gmax<LPR>(maxs);
+        lo[r] = gmin<LPR>(lo[r]);
+        hi[r] = gmax<LPR>(hi[r]);
+        flag[r] = valid && (a.nocache || maxd > __fmul_rn(a.eps, maxs));
+        bal[r] = __ballot_sync(0xffffffffu, flag[r] && gl == 0);
+        if (valid && gl == 0) h.gflag[mrow] = flag[r] ? 1 : 0;
     }
-    maxd = gmax<LPR>(maxd);
-    maxs = gmax<LPR>(maxs);
-    lo = gmin<LPR>(lo);
-    hi = gmax<LPR>(hi);
-    const bool flag = valid && (a.nocache || maxd > __fmul_rn(a.eps, maxs));
-    const unsigned bal = __ballot_sync(0xffffffffu, flag && gl == 0);
-    if (lane == 0) s_wcnt[warp] = __popc(bal);
+    int wcnt = 0;
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) wcnt += __popc(bal[r]);
+    if (lane == 0) s_wcnt[warp] = wcnt;
     __syncthreads();
     if (warp == 0) {
         uint32_t cnt = 0;
@@ -194,56 +211,61 @@ __global__ void __launch_bounds__(kThreads) gather_pack_kernel(HaloDev h, SyncAr
         }
     }
     __syncthreads();
-    int woff = 0;
-    for (int w = 0; w < warp; ++w) woff += s_wcnt[w];
-    const int lead = g * LPR;
-    const int rank_in_warp = __popc(bal & ((1u << lead) - 1u));
-    const int64_t m = (int64_t)s_excl + woff + rank_in_warp;
-    if (valid && gl == 0) h.gflag[mrow] = flag ? 1 : 0;
-    if (!flag) return;
+    int64_t m = (int64_t)s_excl;
+    for (int w = 0; w < warp; ++w) m += s_wcnt[w];
     uint8_t* hdr = h.gsend->hdr[seg];
     uint8_t* pay = h.gsend->pay[seg];
-    if (h.quant) {
-        const float rng = __fsub_rn(hi, lo);
-        const float stp = step8(lo, hi);
-        if (gl == 0) {
-            uint32_t* hp = reinterpret_cast<uint32_t*>(hdr + m * 12);
-            hp[0] = (uint32_t)ridx;
-            hp[1] = __float_as_uint(lo);
-            hp[2] = __float_as_uint(hi);
-        }
-        uint8_t* codes = pay + m * (int64_t)a.F;
+    const int lead = g * LPR;
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-            const int c0 = (gl + v * LPR) * 4;
-            if (c0 >= a.F) continue;
-            uint32_t q[4];
-            float4 snew = make_float4(0.f, 0.f, 0.f, 0.f);
-            float4 s4 = sr ? ld4(sr + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                q[k] = q8(comp(d[v], k), lo, rng);
-                const float sk = (c0 + k < a.F) ? __fadd_rn(comp(s4, k), dq8(q[k], lo, stp)) : 0.f;
-                setc(snew, k, sk);
+    for (int r = 0; r < RPW; ++r) {
+        const int64_t mm = m + __popc(bal[r] & ((1u << lead) - 1u));
+        m += __popc(bal[r]);
+        if (!flag[r]) continue;
+        const int64_t mrow = s_moff[seg] + ridx[r];
+        float* sr = a.nocache ? nullptr : a.c.s_mir + mrow * a.ld;
+        if (h.quant) {
+            const float rng = __fsub_rn(hi[r], lo[r]);
+            const float stp = step8(lo[r], hi[r]);
+            if (gl == 0) {
+                uint32_t* hp = reinterpret_cast<uint32_t*>(hdr + mm * 12);
+                hp[0] = (uint32_t)ridx[r];
+                hp[1] = __float_as_uint(lo[r]);
+                hp[2] = __float_as_uint(hi[r]);
             }
-            if ((a.F & 3) == 0) {
-                *reinterpret_cast<uint32_t*>(codes + c0) = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
-            } else {
+            uint8_t* codes = pay + mm * (int64_t)a.F;
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (c0 + k < a.F) codes[c0 + k] = (uint8_t)q[k];
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 >= a.F) continue;
+                uint32_t q[4];
+                float4 snew = make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 s4 = sr ? ld4(sr + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    q[k] = q8(comp(d[r][v], k), lo[r], rng);
+                    const float sk = (c0 + k < a.F) ? __fadd_rn(comp(s4, k), dq8(q[k], lo[r], stp)) : 0.f;
+                    setc(snew, k, sk);
+                }
+                if ((a.F & 3) == 0) {
+                    *reinterpret_cast<uint32_t*>(codes + c0) = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (c0 + k < a.F) codes[c0 + k] = (uint8_t)q[k];
+                }
+                if (sr) st4(sr + c0, snew);     // reading R11: s ← s + deq(q(Δ))
             }
-            if (sr) st4(sr + c0, snew);     // reading R11: s ← s + deq(q(Δ))
-        }
-    } else {
-        if (gl == 0) reinterpret_cast<uint32_t*>(hdr)[m] = (uint32_t)ridx;
-        float* prow = reinterpret_cast<float*>(pay) + m * a.ld;
+        } else {
+            if (gl == 0) reinterpret_cast<uint32_t*>(hdr)[mm] = (uint32_t)ridx[r];
+            float* prow = reinterpret_cast<float*>(pay) + mm * a.ld;
+            const float* xr = a.X + (h.B + mrow) * a.ld;
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-            const int c0 = (gl + v * LPR) * 4;
-            if (c0 >= a.ld) continue;
-            st4(prow + c0, d[v]);
-            if (sr) st4(sr + c0, x[v]);   // Alg. 2 L6: s ← z
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 >= a.ld) continue;
+                st4(prow + c0, d[r][v]);
+                if (sr) st4(sr + c0, ld4(xr + c0));   // Alg. 2 L6: s ← z
+            }
         }
     }
     if (h.remote) __threadfence_system();   // pushed to a peer GPU: visible before the barrier
@@ -583,6 +605,32 @@ __global__ void __launch_bounds__(kThreads) mirror_apply_kernel(HaloDev h, SyncA
     }
 }
 
+// ==================================================================================
+// put: bulk copy of compacted messages into peer GPUs (16-byte stores over NVLink)
+// ==================================================================================
+__device__ __forceinline__ void copy_bytes(uint8_t* dst, const uint8_t* src, int64_t n, int64_t tid,
+                                           int64_t nthreads) {
+    // both 256-byte aligned region starts; n arbitrary
+    const int64_t n16 = n / 16;
+    const int4* s4 = reinterpret_cast<const int4*>(src);
+    int4* d4 = reinterpret_cast<int4*>(dst);
+    for (int64_t i = tid; i < n16; i += nthreads) d4[i] = s4[i];
+    for (int64_t i = n16 * 16 + tid; i < n; i += nthreads) dst[i] = src[i];
+}
+
+__global__ void put_kernel(const PutTab* __restrict__ tab, int64_t hdr_bytes, int64_t row_bytes) {
+    const int q = blockIdx.y;
+    uint8_t* dh = tab->dst_hdr[q];
+    if (!dh) return;
+    const int64_t cnt = *tab->src_cnt[q];
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    copy_bytes(dh, tab->src_hdr[q], cnt * hdr_bytes, tid, nth);
+    copy_bytes(tab->dst_pay[q], tab->src_pay[q], cnt * row_bytes, tid, nth);
+    if (tid == 0) *tab->dst_cnt[q] = (int32_t)cnt;
+    __threadfence_system();
+}
+
 // ---- dispatch by row width: LPR lanes x VPL float4 per lane cover ld columns ------
 struct Shape { int lpr, vpl; };
 Shape shape_of(int64_t ld) {
@@ -595,6 +643,13 @@ Shape shape_of(int64_t ld) {
     if (nv <= 64) return {32, 2};
     if (nv <= 128) return {32, 4};
     return {32, 8};   // ld <= 1024
+}
+
+// rows per warp pass of gather_pack (must match the launch dispatch below)
+int gather_rpw(int lpr, int vpl) {
+    if (lpr == 16) return 2;
+    if (lpr < 32) return 1;
+    return vpl <= 2 ? 4 : (vpl == 4 ? 2 : 1);
 }
 
 #define CDF_DISPATCH(LD, KERNEL, GRID, STREAM, ...)                                         \
@@ -613,7 +668,8 @@ Shape shape_of(int64_t ld) {
 }  // namespace
 
 int gather_tiles_host(const int64_t* moff, int p, int64_t ld) {
-    const int TR = kWarps * (32 / shape_of(ld).lpr);
+    const Shape sh = shape_of(ld);
+    const int TR = kWarps * (32 / sh.lpr) * gather_rpw(sh.lpr, sh.vpl);
     int t = 0;
     for (int j = 0; j < p; ++j) t += (int)((moff[j + 1] - moff[j] + TR - 1) / TR);
     return t;
@@ -626,8 +682,24 @@ int scatter_tiles_host(const int64_t* hoff, int p) {
 
 int launch_gather_pack_n(const HaloDev& h, const SyncArgs& a, int ntiles, cudaStream_t s) {
     if (ntiles <= 0) return 0;
-    auto grid = [&](int) { return ntiles; };
-    CDF_DISPATCH(a.ld, gather_pack_kernel, grid, s, h, a);
+    const Shape sh = shape_of(a.ld);
+    if (sh.lpr == 2) gather_pack_kernel<2, 1, 1><<<ntiles, kThreads, 0, s>>>(h, a);
+    else if (sh.lpr == 4) gather_pack_kernel<4, 1, 1><<<ntiles, kThreads, 0, s>>>(h, a);
+    else if (sh.lpr == 8) gather_pack_kernel<8, 1, 1><<<ntiles, kThreads, 0, s>>>(h, a);
+    else if (sh.lpr == 16) gather_pack_kernel<16, 1, 2><<<ntiles, kThreads, 0, s>>>(h, a);
+    else if (sh.vpl == 1) gather_pack_kernel<32, 1, 4><<<ntiles, kThreads, 0, s>>>(h, a);
+    else if (sh.vpl == 2) gather_pack_kernel<32, 2, 4><<<ntiles, kThreads, 0, s>>>(h, a);
+    else if (sh.vpl == 4) gather_pack_kernel<32, 4, 2><<<ntiles, kThreads, 0, s>>>(h, a);
+    else gather_pack_kernel<32, 8, 1><<<ntiles, kThreads, 0, s>>>(h, a);
+    return 1;
+}
+
+int launch_put(const PutTab* tab, int p, int64_t hdr_bytes, int64_t row_bytes, int64_t max_count,
+               cudaStream_t s) {
+    if (p <= 1 || max_count <= 0) return 0;
+    const int64_t bytes = max_count * (hdr_bytes + row_bytes);
+    const unsigned bx = (unsigned)std::min<int64_t>(std::max<int64_t>((bytes / 16 + 255) / 256, 1), 296);
+    put_kernel<<<dim3(bx, p), 256, 0, s>>>(tab, hdr_bytes, row_bytes);
     return 1;
 }
 
