@@ -297,6 +297,11 @@ def main(args):
         if dist is not None:
             dist.destroy_process_group()
         return 0
+    # L2 read bandwidth on this GPU (the gather-bound SpMM's real ceiling): 64 MB resident buffer
+    from paper_2408_00232_b200.api import bandwidth_probe
+    probe = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    l2_gbs = bandwidth_probe(probe, 64 << 20, 64)
+    del probe
     peaks, src = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
     sp_ld = stats[-1]["spmm_ld"]
@@ -341,6 +346,8 @@ def main(args):
                      "avg_launch_ms": round(avg_launch_ms, 4) if avg_launch_ms else None,
                      "dram_gbs": round(traffic / (avg_launch_ms * 1e-3) / 1e9, 1)
                      if (traffic and avg_launch_ms) else None,
+                     "l2_read_gbs_probe": round(l2_gbs, 1),
+                     "frac_of_l2": round(achieved / l2_gbs, 4) if achieved else None,
                      "launches": sp_n},
         "gpu_launches": launches,
         "prep_s": round(t_prep, 1),

@@ -262,6 +262,12 @@ int cdfgnn_set_eps(cdfgnn_ctx* ctx, double eps);
 int cdfgnn_spmm(cdfgnn_ctx* ctx, int32_t local_part, const float* T, float* Y, int64_t ld,
                 int32_t F, void* stream);
 
+/* Measurement helper (bench.py roofline): stream `reps` passes of 16-byte reads over
+ * `bytes` of the device buffer `buf` (caller-owned) on `stream`; *gbs = bytes*reps/time.
+ * A buffer that fits the 126 MB L2 measures the L2 read bandwidth the gather-bound
+ * SpMM is limited by; a multi-GB buffer measures HBM read bandwidth. Synchronises. */
+int cdfgnn_bandwidth_probe(const void* buf, int64_t bytes, int32_t reps, double* gbs, void* stream);
+
 const char* cdfgnn_last_error(void);
 const char* cdfgnn_version(void);
 

@@ -123,6 +123,7 @@ _sig("cdfgnn_reset_caches", c_i32, [c_void_p, c_void_p])
 _sig("cdfgnn_get_eps", c_i32, [c_void_p, P(c_f64), P(c_f64)])
 _sig("cdfgnn_set_eps", c_i32, [c_void_p, c_f64])
 _sig("cdfgnn_spmm", c_i32, [c_void_p, c_i32, c_void_p, c_void_p, c_i64, c_i32, c_void_p])
+_sig("cdfgnn_bandwidth_probe", c_i32, [c_void_p, c_i64, c_i32, P(c_f64), c_void_p])
 _sig("cdfgnn_last_error", ctypes.c_char_p, [])
 _sig("cdfgnn_version", ctypes.c_char_p, [])
 

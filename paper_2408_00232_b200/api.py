@@ -281,3 +281,11 @@ def set_eps(ctx: Ctx, eps: float):
 
 def spmm(ctx: Ctx, local_part: int, T, Y, ld: int, F: int, stream=None):
     check(_c.cdfgnn_spmm(ctx.handle, local_part, _ptr(T), _ptr(Y), ld, F, _stream(stream)))
+
+
+def bandwidth_probe(buf, bytes_: int, reps: int, stream=None) -> float:
+    """cdfgnn_bandwidth_probe: GB/s of streaming 16-byte reads over `bytes_` of `buf`."""
+    out = L.c_f64()
+    check(_c.cdfgnn_bandwidth_probe(ctypes.c_void_p(buf.data_ptr()), bytes_, reps, ctypes.byref(out),
+                                    _stream(stream)))
+    return out.value

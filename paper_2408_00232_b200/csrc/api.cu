@@ -1168,5 +1168,26 @@ extern "C" int cdfgnn_spmm(cdfgnn_ctx* c, int32_t lp, const float* T, float* Y, 
     return check_launch("spmm");
 }
 
+extern "C" int cdfgnn_bandwidth_probe(const void* buf, int64_t bytes, int32_t reps, double* gbs, void* stream) {
+    if (!buf || !gbs || bytes < 16 || reps < 1) CDF_FAIL(CDFGNN_EUSAGE, "bad probe arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    const float4* p = reinterpret_cast<const float4*>(buf);
+    const int64_t n4 = bytes / 16;
+    launch_read_probe(p, n4, 1, nullptr, s);    // warm (L2-resident for small buffers)
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    CUDA_TRY(cudaEventRecord(e0, s));
+    launch_read_probe(p, n4, reps, nullptr, s);
+    CUDA_TRY(cudaEventRecord(e1, s));
+    CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *gbs = (double)n4 * 16.0 * reps / (ms * 1e-3) / 1e9;
+    return check_launch("probe");
+}
+
 extern "C" const char* cdfgnn_last_error(void) { return cdfgnn::g_err.c_str(); }
 extern "C" const char* cdfgnn_version(void) { return "cdfgnn-b200 0.1 (sm_100a)"; }

@@ -228,7 +228,21 @@ __global__ void optimizer_kernel(int kind, float* __restrict__ W, const float* _
     W[i] = W[i] - (lr / bc1) * (mi / denom);
 }
 
+__global__ void read_probe_kernel(const float4* __restrict__ p, int64_t n4, int reps, float* sink) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = 0; r < reps; ++r)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+            const float4 v = __ldcg(p + i);
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+    if (acc.x == 1.2345e-30f && sink) sink[0] = acc.y + acc.z + acc.w;   // keep the loads alive
+}
+
 }  // namespace
+
+void launch_read_probe(const float4* p, int64_t n4, int reps, float* sink, cudaStream_t s) {
+    read_probe_kernel<<<148 * 8, 256, 0, s>>>(p, n4, reps, sink);
+}
 
 void launch_gemm_simt(bool TA, bool TB, int64_t M, int64_t N, int64_t K, const float* A,
                       int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
