@@ -93,9 +93,6 @@ struct LocalPart {
     int32_t *idxmap = nullptr, *mmap = nullptr;
     uint8_t* stage_codes = nullptr;
     float *stage_lohi = nullptr, *stage_a = nullptr;
-    unsigned long long *status_g = nullptr, *status_s = nullptr, *ticket = nullptr;
-    unsigned long long tbase_g = 0, tbase_s = 0;
-    uint32_t seq = 0;
     CacheDev cache[CDFGNN_MAX_LAYERS][2] = {};
     float* act[CDFGNN_MAX_LAYERS + 1] = {};
     float *T = nullptr, *S = nullptr, *D[2] = {nullptr, nullptr}, *rowloss = nullptr;
@@ -241,11 +238,6 @@ void carve(cdfgnn_ctx* c, Bump& b) {
         P.stage_codes = b.take<uint8_t>(P.B * c->Fmax);
         P.stage_lohi = b.take<float>(2 * P.B);
         P.stage_a = b.take<float>(P.B * c->ldmax);
-        int64_t tg = 0;
-        for (int j = 0; j < p; ++j) tg += (P.capA[j] + 7) / 8;
-        P.status_g = b.take<unsigned long long>(tg + 1);
-        P.status_s = b.take<unsigned long long>(scatter_tiles_host(P.hoff.data(), p) + 1);
-        P.ticket = b.take<unsigned long long>(2);
         for (int l = 1; l <= L; ++l) {
             const int64_t ld = ld_of(c->cfg.dims[l]);
             for (int dir = 0; dir < 2; ++dir) {
@@ -353,7 +345,6 @@ void build_tables(cdfgnn_ctx* c) {
         h.gflag = P.gflag; h.fired = P.fired; h.active = P.active;
         h.idxmap = P.idxmap; h.mmap = P.mmap;
         h.stage_codes = P.stage_codes; h.stage_lohi = P.stage_lohi; h.stage_a = P.stage_a;
-        h.status_g = P.status_g; h.status_s = P.status_s; h.ticket = P.ticket;
         h.err = c->scal_d + 1;
     }
 }
@@ -526,16 +517,14 @@ int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float 
         a.nocache = c->cfg.cache_on ? 0 : 1;
         a.c = P.cache[l - 1][dir];
         a.stats = c->stats_d + ((l - 1) * 2 + dir) * 4;
-        a.seq = ++P.seq;
     }
     const int64_t rowb = c->cfg.quant_bits ? F : 4 * ld;
     // ---- gather: mirrors test, quantise, pack (Alg. 2 L3-L9)
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
         const int nt = gather_tiles_host(P.moff.data(), p, ld);
-        args[t].ticket_base_g = P.tbase_g;
+        CUDA_TRY(cudaMemsetAsync(P.cnt, 0, sizeof(int32_t) * p, s));       // range reservations
         c->launches += launch_gather_pack_n(P.halo, args[t], nt, s);
-        P.tbase_g += nt;
     }
     CDF_TRY(check_launch("gather_pack"));
     mark(c, PH_SYNC, s, SS_GXFER);
@@ -562,9 +551,8 @@ int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float 
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
         const int nt = scatter_tiles_host(P.hoff.data(), p);
-        args[t].ticket_base_s = P.tbase_s;
+        CUDA_TRY(cudaMemsetAsync(P.cnt + 2 * p, 0, sizeof(int32_t) * p, s));
         c->launches += launch_scatter_pack_n(P.halo, args[t], nt, s);
-        P.tbase_s += nt;
     }
     CDF_TRY(check_launch("scatter_pack"));
     mark(c, PH_SYNC, s, SS_SXFER);

@@ -43,9 +43,6 @@ struct HaloDev {
     uint8_t* stage_codes;      // [B*Fmax] quantised scatter codes
     float* stage_lohi;         // [B*2]
     float* stage_a;            // [B*ldmax] aggregate for the no-cache fp32 scatter
-    unsigned long long* status_g;   // gather tile status words
-    unsigned long long* status_s;   // scatter tile status words
-    unsigned long long* ticket;     // [2] tile tickets (gather, scatter)
     int32_t* err;              // protocol error flag (device)
 };
 
@@ -79,8 +76,6 @@ struct SyncArgs {
     int nocache;          // reading R14
     CacheDev c;
     unsigned long long* stats;  // [4]: gather_sent, master_fired, active, scatter_msgs
-    unsigned long long ticket_base_g, ticket_base_s;
-    uint32_t seq;
 };
 
 // ---- halo kernels (kernels_halo.cu)

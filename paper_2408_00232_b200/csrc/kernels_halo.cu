@@ -3,14 +3,17 @@
 // One synchronisation (§3.2, Alg. 2, §5):
 //   gather_pack   mirrors: d = z − s; send iff max|d| > RN(ε·max|s|) (Alg. 2 L4, reading R15);
 //                 quantise d to uint8 codes per vertex (lo, hi header, §5), compact the
-//                 senders per master peer (warp ballot + block scan + decoupled look-back,
-//                 order preserved), update the snapshot s += deq (reading R11)
+//                 senders per master peer (warp ballot + block prefix + one atomic range
+//                 reservation per block), update the snapshot s += deq (reading R11)
 //   map           received message -> row index tables
 //   master        per boundary master: a += deq(Δ) in ascending source part (Alg. 2
 //                 L11-L13, R13), own test + a += z − s (L14-L19), active flag, scatter
 //                 delta q(a − b) staged once, b += deq (R12), Z row ← b
 //   scatter_pack  per mirror peer: compact active masters, copy staged codes / a
 //   mirror_apply  b += deq (or b ← a), Z row ← b
+// Messages carry their halo-list position, every row receives at most one message per
+// source and masters add sources in ascending order, so results do not depend on the
+// order blocks reserve their ranges in a message buffer (bitwise-deterministic outputs).
 // Every floating-point step of the cache test and the quantiser uses explicit
 // round-to-nearest intrinsics (no FMA contraction) in the canonical order of
 // reading R15, so masks and codes are bit-identical to oracle/cache.py's fp32 replay.
@@ -66,51 +69,6 @@ __device__ __forceinline__ void setc(float4& v, int k, float x) {
     if (k == 0) v.x = x; else if (k == 1) v.y = x; else if (k == 2) v.z = x; else v.w = x;
 }
 
-// ---- decoupled look-back over tiles of one segment ------------------------------
-// status word: [63:32] launch sequence, [31:30] 1 = aggregate, 2 = inclusive prefix, [29:0] value
-__device__ __forceinline__ unsigned long long mkstat(uint32_t seq, uint32_t kind, uint32_t v) {
-    return ((unsigned long long)seq << 32) | ((unsigned long long)kind << 30) | (v & 0x3FFFFFFFu);
-}
-// Called by a whole warp; returns (to every lane) the exclusive prefix of `tile` within its
-// segment.  Lanes inspect 32 predecessors per round (decoupled look-back): the window's
-// aggregates are summed up to the closest inclusive prefix.  Tiles are numbered by a
-// ticket taken when the block starts, so every predecessor is running or done.
-__device__ uint32_t lookback_warp(unsigned long long* status, int tile, bool first_in_seg,
-                                  uint32_t count, uint32_t seq, int lane) {
-    if (lane == 0) {
-        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(status[tile]);
-        me.store(mkstat(seq, first_in_seg ? 2u : 1u, count), cuda::memory_order_release);
-    }
-    if (first_in_seg) return 0;
-    uint32_t excl = 0;
-    int j = tile - 1;
-    while (true) {
-        const int idx = j - lane;
-        unsigned long long w = mkstat(seq, 2, 0);            // below tile 0: empty prefix
-        if (idx >= 0) {
-            cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[idx]);
-            bool ready;
-            do {
-                w = st.load(cuda::memory_order_acquire);
-                ready = (uint32_t)(w >> 32) == seq && ((w >> 30) & 3u) != 0u;
-            } while (!ready);
-        }
-        const unsigned isp = __ballot_sync(0xffffffffu, ((w >> 30) & 3u) == 2u);
-        const int stop = isp ? __ffs(isp) - 1 : 31;           // closest inclusive prefix
-        uint32_t v = lane <= stop ? (uint32_t)(w & 0x3FFFFFFFu) : 0u;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        excl += v;
-        if (isp) break;
-        j -= 32;
-    }
-    if (lane == 0) {
-        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(status[tile]);
-        me.store(mkstat(seq, 2, excl + count), cuda::memory_order_release);
-    }
-    return excl;
-}
-
 __device__ __forceinline__ int find_seg(const int64_t* off, int p, int64_t idx) {
     int s = 0;
     while (s + 1 < p && off[s + 1] <= idx) ++s;
@@ -127,16 +85,13 @@ template <int LPR, int VPL, int RPW>
 __global__ void __launch_bounds__(kThreads) gather_pack_kernel(HaloDev h, SyncArgs a) {
     constexpr int GPW = 32 / LPR;
     constexpr int TR = kWarps * GPW * RPW;
-    __shared__ int s_tile;
     __shared__ int s_wcnt[kWarps];
     __shared__ uint32_t s_excl;
     __shared__ int64_t s_moff[kMaxParts + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x <= h.p) s_moff[threadIdx.x] = h.moff[threadIdx.x];
-    if (threadIdx.x == 0)
-        s_tile = (int)(atomicAdd(&h.ticket[0], 1ull) - a.ticket_base_g);
     __syncthreads();
-    const int tile = s_tile;
+    const int tile = blockIdx.x;
     // segment (master peer) of this tile
     int seg = 0, tbase = 0;
     for (int j = 0; j < h.p; ++j) {
@@ -196,19 +151,11 @@ __global__ void __launch_bounds__(kThreads) gather_pack_kernel(HaloDev h, SyncAr
     for (int r = 0; r < RPW; ++r) wcnt += __popc(bal[r]);
     if (lane == 0) s_wcnt[warp] = wcnt;
     __syncthreads();
-    if (warp == 0) {
+    if (threadIdx.x == 0) {
         uint32_t cnt = 0;
         for (int w = 0; w < kWarps; ++w) cnt += s_wcnt[w];
-        const int ntiles_seg = (int)((seg_len + TR - 1) / TR);
-        const uint32_t excl = lookback_warp(h.status_g, tile, ltile == 0, cnt, a.seq, lane);
-        if (lane == 0) {
-            s_excl = excl;
-            if (ltile == ntiles_seg - 1) {
-                *h.gsend->cnt[seg] = (int32_t)(excl + cnt);
-                if (h.remote) __threadfence_system();
-                atomicAdd(&a.stats[0], (unsigned long long)(excl + cnt));
-            }
-        }
+        s_excl = cnt ? (uint32_t)atomicAdd(h.gsend->cnt[seg], (int32_t)cnt) : 0u;
+        if (cnt) atomicAdd(&a.stats[0], (unsigned long long)cnt);
     }
     __syncthreads();
     int64_t m = (int64_t)s_excl;
@@ -469,7 +416,6 @@ __global__ void __launch_bounds__(kThreads) master_kernel(HaloDev h, SyncArgs a)
 // scatter_pack: one tile = 256 halo-list entries of one mirror peer
 // ==================================================================================
 __global__ void __launch_bounds__(kThreads) scatter_pack_kernel(HaloDev h, SyncArgs a) {
-    __shared__ int s_tile;
     __shared__ int s_wcnt[kWarps];
     __shared__ uint32_t s_excl;
     __shared__ int32_t s_row[kScatterTile];
@@ -477,9 +423,8 @@ __global__ void __launch_bounds__(kThreads) scatter_pack_kernel(HaloDev h, SyncA
     __shared__ int64_t s_hoff[kMaxParts + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x <= h.p) s_hoff[threadIdx.x] = h.hoff[threadIdx.x];
-    if (threadIdx.x == 0) s_tile = (int)(atomicAdd(&h.ticket[1], 1ull) - a.ticket_base_s);
     __syncthreads();
-    const int tile = s_tile;
+    const int tile = blockIdx.x;
     int seg = 0, tbase = 0;
     for (int j = 0; j < h.p; ++j) {
         int64_t len = s_hoff[j + 1] - s_hoff[j];
@@ -496,19 +441,11 @@ __global__ void __launch_bounds__(kThreads) scatter_pack_kernel(HaloDev h, SyncA
     const unsigned bal = __ballot_sync(0xffffffffu, flag);
     if (lane == 0) s_wcnt[warp] = __popc(bal);
     __syncthreads();
-    if (warp == 0) {
+    if (threadIdx.x == 0) {
         uint32_t cnt = 0;
         for (int w = 0; w < kWarps; ++w) cnt += s_wcnt[w];
-        const int ntiles_seg = (int)((seg_len + kScatterTile - 1) / kScatterTile);
-        const uint32_t excl = lookback_warp(h.status_s, tile, ltile == 0, cnt, a.seq, lane);
-        if (lane == 0) {
-            s_excl = excl;
-            if (ltile == ntiles_seg - 1) {
-                *h.ssend->cnt[seg] = (int32_t)(excl + cnt);
-                if (h.remote) __threadfence_system();
-                atomicAdd(&a.stats[3], (unsigned long long)(excl + cnt));
-            }
-        }
+        s_excl = cnt ? (uint32_t)atomicAdd(h.ssend->cnt[seg], (int32_t)cnt) : 0u;
+        if (cnt) atomicAdd(&a.stats[3], (unsigned long long)cnt);
     }
     int woff = 0;
     for (int w = 0; w < warp; ++w) woff += s_wcnt[w];
@@ -519,25 +456,47 @@ __global__ void __launch_bounds__(kThreads) scatter_pack_kernel(HaloDev h, SyncA
     for (int w = 0; w < kWarps; ++w) total += s_wcnt[w];
     uint8_t* hdr = h.ssend->hdr[seg];
     uint8_t* pay = h.ssend->pay[seg];
-    // one warp per message
-    for (int k = warp; k < total; k += kWarps) {
-        const int64_t m = (int64_t)s_excl + k;
+    const int64_t m0 = (int64_t)s_excl;       // this block's contiguous range of messages
+    // headers: one thread per message
+    for (int k = threadIdx.x; k < total; k += kThreads) {
         const int32_t rr = s_row[k];
         if (h.quant) {
-            if (lane == 0) {
-                uint32_t* hp = reinterpret_cast<uint32_t*>(hdr + m * 12);
-                hp[0] = (uint32_t)s_pos[k];
-                hp[1] = __float_as_uint(h.stage_lohi[2 * rr]);
-                hp[2] = __float_as_uint(h.stage_lohi[2 * rr + 1]);
-            }
-            const uint8_t* src = h.stage_codes + (int64_t)rr * a.F;
-            uint8_t* dst = pay + m * (int64_t)a.F;
-            for (int c = lane; c < a.F; c += 32) dst[c] = src[c];
+            uint32_t* hp = reinterpret_cast<uint32_t*>(hdr + (m0 + k) * 12);
+            hp[0] = (uint32_t)s_pos[k];
+            hp[1] = __float_as_uint(h.stage_lohi[2 * rr]);
+            hp[2] = __float_as_uint(h.stage_lohi[2 * rr + 1]);
         } else {
-            if (lane == 0) reinterpret_cast<uint32_t*>(hdr)[m] = (uint32_t)s_pos[k];
-            const float* src = (a.nocache ? h.stage_a : a.c.a) + (int64_t)rr * a.ld;
-            float* dst = reinterpret_cast<float*>(pay) + m * a.ld;
-            for (int c = lane * 4; c < a.ld; c += 128) st4(dst + c, ld4(src + c));
+            reinterpret_cast<uint32_t*>(hdr)[m0 + k] = (uint32_t)s_pos[k];
+        }
+    }
+    // payloads: the block's destination range is contiguous, so the copy is flattened over
+    // (message, word) with coalesced stores
+    if (h.quant) {
+        const int F = a.F;
+        if ((F & 3) == 0) {
+            const int wpr = F >> 2;
+            uint32_t* dst = reinterpret_cast<uint32_t*>(pay + m0 * (int64_t)F);
+            const int64_t nw = (int64_t)total * wpr;
+            for (int64_t i = threadIdx.x; i < nw; i += kThreads) {
+                const int k = (int)(i / wpr), o = (int)(i - (int64_t)k * wpr);
+                dst[i] = reinterpret_cast<const uint32_t*>(h.stage_codes + (int64_t)s_row[k] * F)[o];
+            }
+        } else {
+            uint8_t* dst = pay + m0 * (int64_t)F;
+            const int64_t nb = (int64_t)total * F;
+            for (int64_t i = threadIdx.x; i < nb; i += kThreads) {
+                const int k = (int)(i / F), o = (int)(i - (int64_t)k * F);
+                dst[i] = h.stage_codes[(int64_t)s_row[k] * F + o];
+            }
+        }
+    } else {
+        const float* srcb = a.nocache ? h.stage_a : a.c.a;
+        const int vpr = (int)(a.ld >> 2);
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(pay) + m0 * a.ld);
+        const int64_t nv = (int64_t)total * vpr;
+        for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
+            const int k = (int)(i / vpr), o = (int)(i - (int64_t)k * vpr);
+            dst[i] = reinterpret_cast<const float4*>(srcb + (int64_t)s_row[k] * a.ld)[o];
         }
     }
     if (h.remote) __threadfence_system();
