@@ -221,7 +221,7 @@ def main(args):
             "nocache": (False, 0)}[args.mode]
     run = Run(ds, world, rank=rank, world=world, device=local, cache=mode[0], quant_bits=mode[1],
               eps0=args.eps0, adaptive=True, optimizer="adam", lr=0.01, timing=True,
-              host_inputs=not args.no_e2e, transport=args.transport)
+              host_inputs=not args.no_e2e, transport=args.transport, static_inputs=True)
     t_prep = time.time() - t_prep
     for _ in range(args.warmup):
         run.epoch()

@@ -150,6 +150,12 @@ typedef struct {
                                            one NCCL barrier per phase, no host round trip;
                                            falls back to 1 if IPC is unavailable);
                                            1 = NCCL grouped send/recv after a count exchange */
+    int32_t elide_dead_syncs;           /* 1 (default): inside cdfgnn_epoch skip the layer-L forward
+                                           scatter and backward gather (§8 f2; bitwise-identical
+                                           results: mirrors never read logits and their δ̈^(L) = 0) */
+    int32_t static_inputs;              /* 1: the input features X do not change between calls for
+                                           a given buffer, so Xᵀ (∇W^(0) operand) is built once per
+                                           X pointer and reused; 0 (default): rebuilt every epoch */
 } cdfgnn_cfg;
 
 int cdfgnn_cfg_default(cdfgnn_cfg* cfg);

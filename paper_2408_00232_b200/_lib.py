@@ -67,7 +67,8 @@ class CfgC(ctypes.Structure):
                 ("nu1", c_f64), ("nu2", c_f64), ("xi", c_f64), ("lam1", c_f64), ("lam2", c_f64),
                 ("eps_clamp", c_i32), ("quant_bits", c_i32), ("optimizer", c_i32), ("lr", c_f64),
                 ("beta1", c_f64), ("beta2", c_f64), ("adam_eps", c_f64), ("gemm_tf32", c_i32),
-                ("timing", c_i32), ("transport", c_i32)]
+                ("timing", c_i32), ("transport", c_i32), ("elide_dead_syncs", c_i32),
+                ("static_inputs", c_i32)]
 
 
 class SyncStatsC(ctypes.Structure):

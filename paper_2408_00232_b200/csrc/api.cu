@@ -80,6 +80,8 @@ struct LocalPart {
     // device
     int32_t *rowptr = nullptr, *colidx = nullptr, *halo_local = nullptr;
     int32_t* order = nullptr;          // SpMM row order: degree-descending (longest first)
+    float* xT = nullptr;               // cached H^(0)ᵀ (cfg.static_inputs) for ∇W^(0)
+    const float* xT_src = nullptr;     // the X pointer xT was built from
     float* val = nullptr;
     int64_t *moff_d = nullptr, *hoff_d = nullptr;
     uint8_t* regA[kMaxParts] = {};
@@ -275,6 +277,8 @@ void carve(cdfgnn_ctx* c, Bump& b) {
     if (c->cfg.gemm_tf32) {
         c->trA = b.take<float>(c->fin_max * c->npad);
         c->trB = b.take<float>(c->Fmax * c->npad);
+        if (c->cfg.static_inputs)
+            for (LocalPart& P : c->parts) P.xT = b.take<float>((int64_t)c->cfg.dims[0] * ld_of(P.n));
     }
     c->stats_d = b.take<unsigned long long>(CDFGNN_MAX_LAYERS * 2 * 4);
     c->loss_d = b.take<double>(std::max(c->k, 1));
@@ -503,8 +507,11 @@ int setup_push(cdfgnn_ctx* c, cudaStream_t s) {
     return CDFGNN_OK;
 }
 
+// skip_gather / skip_scatter: §8 f2 dead-sync elision inside cdfgnn_epoch — the layer-L
+// forward scatter (mirrors never read logits, the loss is on masters) and the
+// layer-L backward gather (mirrors' δ̈^(L) is identically zero) carry no information.
 int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float eps,
-              cudaStream_t s, int64_t* wire) {
+              cudaStream_t s, int64_t* wire, bool skip_gather = false, bool skip_scatter = false) {
     const int p = c->p;
     const int F = (int)sync_width(c, l);
     if (ld != ld_of(F)) CDF_FAIL(CDFGNN_EUSAGE, "ld %lld must equal roundup(F=%d, 4)", (long long)ld, F);
@@ -517,10 +524,11 @@ int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float 
         a.nocache = c->cfg.cache_on ? 0 : 1;
         a.c = P.cache[l - 1][dir];
         a.stats = c->stats_d + ((l - 1) * 2 + dir) * 4;
+        a.no_msgs = skip_gather ? 1 : 0;
     }
     const int64_t rowb = c->cfg.quant_bits ? F : 4 * ld;
     // ---- gather: mirrors test, quantise, pack (Alg. 2 L3-L9)
-    for (int t = 0; t < c->k; ++t) {
+    for (int t = 0; t < c->k && !skip_gather; ++t) {
         LocalPart& P = c->parts[t];
         const int nt = gather_tiles_host(P.moff.data(), p, ld);
         CUDA_TRY(cudaMemsetAsync(P.cnt, 0, sizeof(int32_t) * p, s));       // range reservations
@@ -528,8 +536,8 @@ int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float 
     }
     CDF_TRY(check_launch("gather_pack"));
     mark(c, PH_SYNC, s, SS_GXFER);
-    if (c->transport == 1) CDF_TRY(nccl_phase(c, c->parts[0], true, rowb, s, wire));
-    if (c->transport == 2) {
+    if (c->transport == 1 && !skip_gather) CDF_TRY(nccl_phase(c, c->parts[0], true, rowb, s, wire));
+    if (c->transport == 2 && !skip_gather) {
         LocalPart& P = c->parts[0];
         c->launches += launch_put(P.putG_d, p, c->hdr_bytes, rowb,
                                   *std::max_element(P.capA.begin(), P.capA.end()), s);
@@ -541,11 +549,14 @@ int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float 
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
         if (P.B == 0) continue;
-        CUDA_TRY(cudaMemsetAsync(P.idxmap, 0xFF, sizeof(int32_t) * p * P.B, s));
-        c->launches += launch_map(P.halo, 0, *std::max_element(P.capB.begin(), P.capB.end()), s);
+        if (!skip_gather) {
+            CUDA_TRY(cudaMemsetAsync(P.idxmap, 0xFF, sizeof(int32_t) * p * P.B, s));
+            c->launches += launch_map(P.halo, 0, *std::max_element(P.capB.begin(), P.capB.end()), s);
+        }
         c->launches += launch_master(P.halo, args[t], s);
     }
     CDF_TRY(check_launch("master"));
+    if (skip_scatter) return CDFGNN_OK;
     mark(c, PH_SYNC, s, SS_SPACK);
     // ---- scatter: active masters to every mirror (L20-L22)
     for (int t = 0; t < c->k; ++t) {
@@ -612,7 +623,7 @@ int spmm_part(cdfgnn_ctx* c, LocalPart& P, const float* T, float* Y, int64_t ld,
 
 int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, const float* W,
              float* const* Z, float* const* H_out, int64_t ld_out, float eps, cudaStream_t s,
-             int64_t* wire) {
+             int64_t* wire, bool elide = false) {
     const int64_t Fi = c->cfg.dims[l - 1], Fo = c->cfg.dims[l];
     if (ld_in < Fi || ld_in % 4 || ld_out != ld_of(Fo)) CDF_FAIL(CDFGNN_EUSAGE, "bad leading dimension");
     float* Wt = c->wtpad + c->wtoff[l - 1];
@@ -634,7 +645,7 @@ int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, cons
         CDF_TRY(check_launch("gemm fwd"));
         CDF_TRY(spmm_part(c, P, P.T, Z[t], ld_out, s));
     }
-    CDF_TRY(halo_impl(c, l, 0, Z, ld_out, eps, s, wire));
+    CDF_TRY(halo_impl(c, l, 0, Z, ld_out, eps, s, wire, false, elide && l == c->cfg.L));
     if (H_out) {
         mark(c, PH_OTHER, s);
         for (int t = 0; t < c->k; ++t) {
@@ -648,10 +659,10 @@ int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, cons
 
 int bwd_impl(cdfgnn_ctx* c, int l, float* const* dZ, int64_t ld, const float* const* H_in,
              int64_t ld_in, const float* W, float* const* dZ_prev, float* dW, float eps,
-             cudaStream_t s, int64_t* wire) {
+             cudaStream_t s, int64_t* wire, bool elide = false) {
     const int64_t Fi = c->cfg.dims[l - 1], Fo = c->cfg.dims[l];
     if (ld != ld_of(Fo) || ld_in < Fi || ld_in % 4) CDF_FAIL(CDFGNN_EUSAGE, "bad leading dimension");
-    CDF_TRY(halo_impl(c, l, 1, dZ, ld, eps, s, wire));
+    CDF_TRY(halo_impl(c, l, 1, dZ, ld, eps, s, wire, elide && l == c->cfg.L, false));
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
         CDF_TRY(spmm_part(c, P, dZ[t], P.S, ld, s));
@@ -659,9 +670,21 @@ int bwd_impl(cdfgnn_ctx* c, int l, float* const* dZ, int64_t ld, const float* co
         // dW (+)= H_inᵀ S ; parts accumulate in ascending order
         if (c->cfg.gemm_tf32) {
             if (t == 0) c->launches += launch_pad_rows(W, Fi, Fo, c->wpad + c->wpoff[l - 1], ld, s);
-            c->launches += launch_transpose(H_in[t], P.n, Fi, ld_in, c->trA, c->npad, s);
+            const float* Ht = c->trA;
+            int64_t ldh = c->npad;
+            if (l == 1 && P.xT) {
+                // static inputs: H^(0)ᵀ = Xᵀ is transposed once per X buffer and reused
+                if (P.xT_src != H_in[t]) {
+                    c->launches += launch_transpose(H_in[t], P.n, Fi, ld_in, P.xT, ld_of(P.n), s);
+                    P.xT_src = H_in[t];
+                }
+                Ht = P.xT;
+                ldh = ld_of(P.n);
+            } else {
+                c->launches += launch_transpose(H_in[t], P.n, Fi, ld_in, c->trA, c->npad, s);
+            }
             c->launches += launch_transpose(P.S, P.n, Fo, ld, c->trB, c->npad, s);
-            CDF_TRY(gemm_tc_wgrad(Fi, Fo, P.n, c->trA, c->npad, c->trB, c->npad, dW, Fo, c->splitk,
+            CDF_TRY(gemm_tc_wgrad(Fi, Fo, P.n, Ht, ldh, c->trB, c->npad, dW, Fo, c->splitk,
                                   c->splitk_cap, t > 0, c->cfg.gemm_tf32 == 3, s, &c->launches));
             if (dZ_prev) {
                 CDF_TRY(gemm_tc_bwd_data(P.n, Fi, Fo, P.S, ld, c->wpad + c->wpoff[l - 1], ld, dZ_prev[t],
@@ -710,6 +733,9 @@ extern "C" int cdfgnn_cfg_default(cdfgnn_cfg* cfg) {
     cfg->lr = 0.01; cfg->beta1 = 0.9; cfg->beta2 = 0.999; cfg->adam_eps = 1e-8;
     cfg->gemm_tf32 = 3;
     cfg->timing = 0;
+    cfg->transport = 0;
+    cfg->elide_dead_syncs = 1;
+    cfg->static_inputs = 0;
     return CDFGNN_OK;
 }
 
@@ -919,7 +945,7 @@ static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const
         std::vector<float*> z(k);
         for (int t = 0; t < k; ++t) z[t] = c->parts[t].act[l];
         CDF_TRY(fwd_impl(c, l, hin.data(), ld_in, W[l - 1], z.data(), l < L ? z.data() : nullptr,
-                         ld, eps32, s, &wire[l - 1][0]));
+                         ld, eps32, s, &wire[l - 1][0], c->cfg.elide_dead_syncs != 0));
         for (int t = 0; t < k; ++t) hin[t] = z[t];
         ld_in = ld;
     }
@@ -946,7 +972,7 @@ static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const
             dprev[t] = c->parts[t].D[(l - 1) & 1];
         }
         CDF_TRY(bwd_impl(c, l, dcur.data(), ld, h.data(), ldi, W[l - 1], l > 1 ? dprev.data() : nullptr,
-                         c->dW + c->woff[l - 1], eps32, s, &wire[l - 1][1]));
+                         c->dW + c->woff[l - 1], eps32, s, &wire[l - 1][1], c->cfg.elide_dead_syncs != 0));
         dcur = dprev;
     }
     // ---- parameter aggregation + update (Alg. 1 L12-L13)

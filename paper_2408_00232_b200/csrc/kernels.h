@@ -74,6 +74,7 @@ struct SyncArgs {
     int F;
     float eps;
     int nocache;          // reading R14
+    int no_msgs;          // gather phase elided (§8 f2): masters see no received messages
     CacheDev c;
     unsigned long long* stats;  // [4]: gather_sent, master_fired, active, scatter_msgs
 };

@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kThreads) master_kernel(HaloDev h, SyncArgs a)
     }
     bool any_msg = false;
     // Alg. 2 L11-L13: received Δ in ascending source part (R13)
-    for (int s = 0; s < h.p; ++s) {
+    for (int s = 0; s < (a.no_msgs ? 0 : h.p); ++s) {
         if (s == h.me) continue;
         const int32_t m = valid ? h.idxmap[(int64_t)s * h.B + r] : -1;
         if (m < 0) continue;

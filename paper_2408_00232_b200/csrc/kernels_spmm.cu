@@ -28,7 +28,7 @@ namespace {
 
 constexpr int kThreads = 256;
 
-template <int LPR, int VPL, int UNR>
+template <int LPR, int VPL, int UNR, int TAIL>
 __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n, const int32_t* __restrict__ rowptr,
                                                         const int32_t* __restrict__ colidx,
                                                         const float* __restrict__ val,
@@ -60,46 +60,81 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n, const int32_t
         const int c = e < end ? __ldg(colidx + e) : 0;
         const float w = e < end ? __ldg(val + e) : 0.f;
         const int cnt = min(LPR, end - base);
-        int k = 0;
-        for (; k + UNR <= cnt; k += UNR) {
-            int ck[UNR];
-            float wk[UNR];
+        if (TAIL == 0) {
+            // full batches of UNR neighbours, then the remainder one at a time
+            int k = 0;
+            for (; k + UNR <= cnt; k += UNR) {
+                int ck[UNR];
+                float wk[UNR];
 #pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                ck[u] = __shfl_sync(gmask, c, k + u, LPR);
-                wk[u] = __shfl_sync(gmask, w, k + u, LPR);
+                for (int u = 0; u < UNR; ++u) {
+                    ck[u] = __shfl_sync(gmask, c, k + u, LPR);
+                    wk[u] = __shfl_sync(gmask, w, k + u, LPR);
+                }
+                float4 t[UNR][VPL];
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const float* tr = Tp + (int64_t)ck[u] * ld;
+#pragma unroll
+                    for (int v = 0; v < VPL; ++v)
+                        t[u][v] = colok[v] ? __ldg(reinterpret_cast<const float4*>(tr + (gl + v * LPR) * 4))
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < UNR; ++u)
+#pragma unroll
+                    for (int v = 0; v < VPL; ++v) {
+                        acc[v].x = fmaf(wk[u], t[u][v].x, acc[v].x);
+                        acc[v].y = fmaf(wk[u], t[u][v].y, acc[v].y);
+                        acc[v].z = fmaf(wk[u], t[u][v].z, acc[v].z);
+                        acc[v].w = fmaf(wk[u], t[u][v].w, acc[v].w);
+                    }
             }
-            float4 t[UNR][VPL];
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const float* tr = Tp + (int64_t)ck[u] * ld;
-#pragma unroll
-                for (int v = 0; v < VPL; ++v)
-                    t[u][v] = colok[v] ? __ldg(reinterpret_cast<const float4*>(tr + (gl + v * LPR) * 4))
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int u = 0; u < UNR; ++u)
+            for (; k < cnt; ++k) {
+                const int ck = __shfl_sync(gmask, c, k, LPR);
+                const float wk = __shfl_sync(gmask, w, k, LPR);
+                const float* tr = Tp + (int64_t)ck * ld;
 #pragma unroll
                 for (int v = 0; v < VPL; ++v) {
-                    acc[v].x = fmaf(wk[u], t[u][v].x, acc[v].x);
-                    acc[v].y = fmaf(wk[u], t[u][v].y, acc[v].y);
-                    acc[v].z = fmaf(wk[u], t[u][v].z, acc[v].z);
-                    acc[v].w = fmaf(wk[u], t[u][v].w, acc[v].w);
+                    if (!colok[v]) continue;
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(tr + (gl + v * LPR) * 4));
+                    acc[v].x = fmaf(wk, t.x, acc[v].x);
+                    acc[v].y = fmaf(wk, t.y, acc[v].y);
+                    acc[v].z = fmaf(wk, t.z, acc[v].z);
+                    acc[v].w = fmaf(wk, t.w, acc[v].w);
                 }
-        }
-        for (; k < cnt; ++k) {
-            const int ck = __shfl_sync(gmask, c, k, LPR);
-            const float wk = __shfl_sync(gmask, w, k, LPR);
-            const float* tr = Tp + (int64_t)ck * ld;
+            }
+        } else {
+            // UNR neighbours per batch; the last, partial batch uses predicated loads so its
+            // neighbours are still in flight together (dead slots add +0)
+            for (int k = 0; k < cnt; k += UNR) {
+                int ck[UNR];
+                float wk[UNR];
 #pragma unroll
-            for (int v = 0; v < VPL; ++v) {
-                if (!colok[v]) continue;
-                const float4 t = __ldg(reinterpret_cast<const float4*>(tr + (gl + v * LPR) * 4));
-                acc[v].x = fmaf(wk, t.x, acc[v].x);
-                acc[v].y = fmaf(wk, t.y, acc[v].y);
-                acc[v].z = fmaf(wk, t.z, acc[v].z);
-                acc[v].w = fmaf(wk, t.w, acc[v].w);
+                for (int u = 0; u < UNR; ++u) {
+                    ck[u] = __shfl_sync(gmask, c, (k + u) & (LPR - 1), LPR);
+                    wk[u] = __shfl_sync(gmask, w, (k + u) & (LPR - 1), LPR);
+                    if (k + u >= cnt) wk[u] = 0.f;
+                }
+                float4 t[UNR][VPL];
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const float* tr = Tp + (int64_t)ck[u] * ld;
+                    const bool live = k + u < cnt;
+#pragma unroll
+                    for (int v = 0; v < VPL; ++v)
+                        t[u][v] = (live && colok[v]) ? __ldg(reinterpret_cast<const float4*>(tr + (gl + v * LPR) * 4))
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < UNR; ++u)
+#pragma unroll
+                    for (int v = 0; v < VPL; ++v) {
+                        acc[v].x = fmaf(wk[u], t[u][v].x, acc[v].x);
+                        acc[v].y = fmaf(wk[u], t[u][v].y, acc[v].y);
+                        acc[v].z = fmaf(wk[u], t[u][v].z, acc[v].z);
+                        acc[v].w = fmaf(wk[u], t[u][v].w, acc[v].w);
+                    }
             }
         }
     }
@@ -111,12 +146,16 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n, const int32_t
 
 template <int LPR, int VPL, int UNR>
 void launch(int64_t n, const int32_t* rowptr, const int32_t* colidx, const float* val, const float* T, float* Y,
-            int64_t ld, int pw, const int32_t* order, cudaStream_t s) {
+            int64_t ld, int pw, const int32_t* order, cudaStream_t s, int tail) {
     const int64_t rows_per_block = (kThreads / 32) * (32 / LPR);
     const int64_t bpp = (n + rows_per_block - 1) / rows_per_block;
     const int64_t panels = (ld + pw - 1) / pw;
-    spmm_kernel<LPR, VPL, UNR><<<(unsigned)(bpp * panels), kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, pw,
-                                                                             bpp, order);
+    if (tail)
+        spmm_kernel<LPR, VPL, UNR, 1><<<(unsigned)(bpp * panels), kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y,
+                                                                                    ld, pw, bpp, order);
+    else
+        spmm_kernel<LPR, VPL, UNR, 0><<<(unsigned)(bpp * panels), kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y,
+                                                                                    ld, pw, bpp, order);
 }
 
 int env_int(const char* name, int dflt) {
@@ -135,21 +174,22 @@ void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val,
     pw = (int)std::min<int64_t>(pw, ld);
     const int nv = pw / 4;      // float4 per row within a panel
     const int unr = env_int("CDFGNN_SPMM_UNR", 0);
-    if (nv <= 2) launch<2, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s);
-    else if (nv <= 4) launch<4, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s);
-    else if (nv <= 8) launch<8, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s);
+    const int tail = env_int("CDFGNN_SPMM_TAIL", ld > 64 ? 1 : 0);   // predicated tail for wide rows
+    if (nv <= 2) launch<2, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
+    else if (nv <= 4) launch<4, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
+    else if (nv <= 8) launch<8, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
     else if (nv <= 16) {
-        if (unr == 4) launch<16, 1, 4>(n, rowptr, colidx, val, T, Y, ld, pw, order, s);
-        else launch<16, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s);
+        if (unr == 4) launch<16, 1, 4>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
+        else launch<16, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
     } else if (nv <= 32) {
-        if (unr == 4) launch<32, 1, 4>(n, rowptr, colidx, val, T, Y, ld, pw, order, s);
-        else launch<32, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s);
+        if (unr == 4) launch<32, 1, 4>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
+        else launch<32, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
     } else if (nv <= 64) {
-        if (unr == 2) launch<32, 2, 2>(n, rowptr, colidx, val, T, Y, ld, pw, order, s);
-        else if (unr == 8) launch<32, 2, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s);
-        else launch<32, 2, 4>(n, rowptr, colidx, val, T, Y, ld, pw, order, s);
-    } else if (nv <= 128) launch<32, 4, 4>(n, rowptr, colidx, val, T, Y, ld, pw, order, s);
-    else launch<32, 8, 2>(n, rowptr, colidx, val, T, Y, ld, pw, order, s);
+        if (unr == 2) launch<32, 2, 2>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
+        else if (unr == 8) launch<32, 2, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
+        else launch<32, 2, 4>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
+    } else if (nv <= 128) launch<32, 4, 4>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
+    else launch<32, 8, 2>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
 }
 
 }  // namespace cdfgnn

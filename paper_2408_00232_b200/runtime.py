@@ -32,7 +32,8 @@ class Run:
                  adaptive: bool = True, optimizer: str = "adam", lr: float = 0.01,
                  timing: bool = False, plan: Optional[api.Plan] = None,
                  host_inputs: bool = False, partition_kw: Optional[Dict] = None,
-                 gemm: str = "tf32x3", transport: str = "push"):
+                 gemm: str = "tf32x3", transport: str = "push", elide: bool = True,
+                 static_inputs: bool = False):
         import torch
         self.torch = torch
         self.ds = ds
@@ -45,7 +46,8 @@ class Run:
                                    eps_init=eps0, adaptive=int(adaptive),
                                    optimizer=1 if optimizer == "adam" else 0, lr=lr,
                                    timing=int(timing), gemm_tf32=GEMM_MODES[gemm],
-                                   transport={"push": 0, "nccl": 1}[transport])
+                                   transport={"push": 0, "nccl": 1}[transport],
+                                   elide_dead_syncs=int(elide), static_inputs=int(static_inputs))
         nbytes = api.workspace_size(self.plan, self.parts, self.cfg)
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         uid = None

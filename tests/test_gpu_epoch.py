@@ -136,3 +136,20 @@ def test_label_out_of_range_is_edata():
         run.epoch()
     assert e.value.code == 3
     run.close()
+
+
+@pytest.mark.parametrize("cache,quant", [(True, 8), (False, 0)])
+def test_dead_sync_elision_and_static_inputs_are_bitwise_neutral(cache, quant):
+    """§8 f2: skipping the layer-L forward scatter and backward gather, and reusing Xᵀ,
+    change no bit of the trajectory."""
+    torch = require_gpu()
+    d = small_random_graph(1200, 8000, (20, 24, 6), seed=65)
+    runs = [Run(d, 3, cache=cache, quant_bits=quant, eps0=0.01, elide=e, static_inputs=si)
+            for e, si in ((False, False), (True, True))]
+    for ep in range(4):
+        res = [r.epoch() for r in runs]
+        assert res[0]["loss"] == res[1]["loss"]
+        for wa, wb in zip(runs[0].weights(), runs[1].weights()):
+            assert np.array_equal(wa, wb)
+    for r in runs:
+        r.close()

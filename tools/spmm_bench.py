@@ -37,6 +37,10 @@ def main():
           kv = dict(x.split(":") for x in var.split(","))
           os.environ["CDFGNN_SPMM_IDENTITY"] = kv.get("id", "0")
           os.environ["CDFGNN_SPMM_UNR"] = kv.get("unr", "0")
+          if "tail" in kv:
+              os.environ["CDFGNN_SPMM_TAIL"] = kv["tail"]
+          else:
+              os.environ.pop("CDFGNN_SPMM_TAIL", None)
           for pw in [int(x) for x in a.panels.split(",")]:
             os.environ["CDFGNN_SPMM_PANEL"] = str(pw)
             ts = []
