@@ -195,3 +195,13 @@ def test_edge_imbalance_small():
     d = small_random_graph(2000, 8000, (4, 3), seed=33)
     st = stats(partition(d.n, d.eu, d.ev, PartitionCfg(p=4)))
     assert st.edge_if < 1.05 and st.vertex_if < 1.05
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_gamma_reduces_outer_connections(seed):
+    """Directional check of P:L799: with 2 hosts x 2 GPUs, γ = 0.1 yields fewer
+    inter-host ("outer") messages than γ = 0 on a power-law graph."""
+    d = small_random_graph(2000, 6000, (4, 3), seed=seed, tau=2.2, v0=5.0)
+    s0 = stats(partition(d.n, d.eu, d.ev, PartitionCfg(p=4, num_hosts=2, gamma=(0, 1))))
+    s1 = stats(partition(d.n, d.eu, d.ev, PartitionCfg(p=4, num_hosts=2, gamma=(1, 10))))
+    assert s1.outer_max < s0.outer_max
