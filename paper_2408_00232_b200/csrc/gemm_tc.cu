@@ -30,7 +30,7 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;            // 32 tf32 = 128 bytes: one swizzle row
-constexpr int kThreads = 192;     // 6 warps: TMA, MMA, 4 x epilogue
+constexpr int kThreads = 320;     // 10 warps: TMA, MMA, 4 x converter, 4 x epilogue
 #ifndef GEMM_MN_LBO
 #define GEMM_MN_LBO (BK * 128)   // MN-major: byte stride between 32-element MN chunks
 #endif
@@ -126,7 +126,7 @@ struct Cfg {
     static constexpr int STAGE_BYTES = TMA_BYTES * (SPLIT3 ? 2 : 1);     // + lo parts for 3xTF32
     static constexpr int STAGES = (SPLIT3 ? 196608 : 200704) / STAGE_BYTES;
     static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-    static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+    static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;        // double-buffered accumulator
 };
 
 __device__ __forceinline__ float tf32_rn(float x) {
@@ -145,10 +145,17 @@ struct EpiArgs {
     int accumulate;
 };
 
+// Persistent, warp-specialised tcgen05 GEMM.  One CTA per SM walks the output tiles
+// (m fastest-changing over n so neighbouring CTAs share A tiles in L2):
+//   warp 0          TMA producer (STAGES-deep smem ring, mbarrier full/empty)
+//   warp 1          MMA issuer (one elected thread), accumulator double-buffered in TMEM
+//                   (2 x BN columns) so the epilogue of tile i overlaps the MMAs of tile i+1
+//   warps 2-5       3xTF32 converters: fp32 tile -> tf32 hi (in place) + lo (second buffer)
+//   warps 6-9       epilogue: tcgen05.ld 32 lanes each -> mask / zero padding / split-K partial
 template <bool A_MN, bool B_MN, int BN, bool SPLIT3>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                 int total_kb, int kb_per_split, EpiArgs ep) {
+                 int total_kb, int kb_per_split, int m_tiles, int n_tiles, int z_tiles, EpiArgs ep) {
     using C_ = Cfg<BN, SPLIT3>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -158,14 +165,12 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C_::STAGES * C_::STAGE_BYTES);
     uint64_t* empty = full + C_::STAGES;
     uint64_t* conv = empty + C_::STAGES;
-    uint64_t* tmem_full = conv + C_::STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* tfull = conv + C_::STAGES;      // [2] accumulator ready
+    uint64_t* tempty = tfull + 2;             // [2] accumulator drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-    const int kb0 = blockIdx.z * kb_per_split;
-    const int kb1 = min(total_kb, kb0 + kb_per_split);
-    const int nkb = kb1 - kb0;
+    const int total_tiles = m_tiles * n_tiles * z_tiles;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < C_::STAGES; ++s) {
@@ -173,7 +178,10 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             mbar_init(&empty[s], 1);
             mbar_init(&conv[s], 4);          // one arrival per converter warp
         }
-        mbar_init(tmem_full, 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);        // one arrival per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -189,30 +197,47 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    auto decode = [&](int t, int& m0, int& n0, int& kb0, int& nkb) {
+        const int mn = m_tiles * n_tiles;
+        const int z = t / mn;
+        const int r = t - z * mn;
+        const int nt = r / m_tiles;
+        const int mt = r - nt * m_tiles;
+        m0 = mt * BM;
+        n0 = nt * BN;
+        kb0 = z * kb_per_split;
+        nkb = min(total_kb, kb0 + kb_per_split) - kb0;
+    };
+
     if (warp == 0) {
         if (lane == 0) {
             // ---------------- TMA producer ----------------
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % C_::STAGES;
-                const uint32_t ph = (uint32_t)(i / C_::STAGES) & 1u;
-                mbar_wait(&empty[s], ph ^ 1u);
-                mbar_expect_tx(&full[s], C_::TMA_BYTES);
-                const int k = (kb0 + i) * BK;
-                uint8_t* a = stA(s);
-                uint8_t* b = stB(s);
-                if (!A_MN) {
-                    tma_load_2d(a, &tmA, &full[s], k, m0);                         // box {32 k, 128 m}
-                } else {
+            int it = 0;
+            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+                int m0, n0, kb0, nkb;
+                decode(t, m0, n0, kb0, nkb);
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % C_::STAGES;
+                    const uint32_t ph = (uint32_t)(it / C_::STAGES) & 1u;
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    mbar_expect_tx(&full[s], C_::TMA_BYTES);
+                    const int k = (kb0 + i) * BK;
+                    uint8_t* a = stA(s);
+                    uint8_t* b = stB(s);
+                    if (!A_MN) {
+                        tma_load_2d(a, &tmA, &full[s], k, m0);                      // box {32 k, 128 m}
+                    } else {
 #pragma unroll
-                    for (int c = 0; c < BM / 32; ++c)                               // box {32 m, 32 k}
-                        tma_load_2d(a + c * BK * 128, &tmA, &full[s], m0 + 32 * c, k);
-                }
-                if (!B_MN) {
-                    tma_load_2d(b, &tmB, &full[s], k, n0);                         // box {32 k, BN n}
-                } else {
+                        for (int c = 0; c < BM / 32; ++c)
+                            tma_load_2d(a + c * BK * 128, &tmA, &full[s], m0 + 32 * c, k);
+                    }
+                    if (!B_MN) {
+                        tma_load_2d(b, &tmB, &full[s], k, n0);                      // box {32 k, BN n}
+                    } else {
 #pragma unroll
-                    for (int c = 0; c < BN / 32; ++c)                               // box {32 n, 32 k}
-                        tma_load_2d(b + c * BK * 128, &tmB, &full[s], n0 + 32 * c, k);
+                        for (int c = 0; c < BN / 32; ++c)
+                            tma_load_2d(b + c * BK * 128, &tmB, &full[s], n0 + 32 * c, k);
+                    }
                 }
             }
         }
@@ -222,120 +247,140 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
                                        ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
                                        ((uint32_t)(BM >> 4) << 24);
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % C_::STAGES;
-                const uint32_t ph = (uint32_t)(i / C_::STAGES) & 1u;
-                mbar_wait(SPLIT3 ? &conv[s] : &full[s], ph);
+            int it = 0, ti = 0;
+            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+                int m0, n0, kb0, nkb;
+                decode(t, m0, n0, kb0, nkb);
+                const int acc = ti & 1;
+                const uint32_t aph = (uint32_t)(ti >> 1) & 1u;
+                mbar_wait(&tempty[acc], aph ^ 1u);         // epilogue drained this accumulator
                 tc_fence_after();
-                const uint32_t a_base = smem_u32(stA(s));
-                const uint32_t b_base = smem_u32(stB(s));
-                if (SPLIT3) {
-                    // 3xTF32: A_hi·B_hi + A_hi·B_lo + A_lo·B_hi
-                    const uint32_t alo = a_base + C_::TMA_BYTES, blo = b_base + C_::TMA_BYTES;
+                const uint32_t dcol = tmem + (uint32_t)(acc * BN);
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % C_::STAGES;
+                    const uint32_t ph = (uint32_t)(it / C_::STAGES) & 1u;
+                    mbar_wait(SPLIT3 ? &conv[s] : &full[s], ph);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(stA(s));
+                    const uint32_t b_base = smem_u32(stB(s));
+                    if (SPLIT3) {
+                        // 3xTF32: A_hi·B_hi + A_hi·B_lo + A_lo·B_hi
+                        const uint32_t alo = a_base + C_::TMA_BYTES, blo = b_base + C_::TMA_BYTES;
 #pragma unroll
-                    for (int kk = 0; kk < BK / 8; ++kk) {
-                        const uint64_t ah = smem_desc(a_base + kk * 32, 16, 1024);
-                        const uint64_t bh = smem_desc(b_base + kk * 32, 16, 1024);
-                        const uint64_t al = smem_desc(alo + kk * 32, 16, 1024);
-                        const uint64_t bl = smem_desc(blo + kk * 32, 16, 1024);
-                        tc_mma_tf32(tmem, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
-                        tc_mma_tf32(tmem, ah, bl, idesc, 1u);
-                        tc_mma_tf32(tmem, al, bh, idesc, 1u);
+                        for (int kk = 0; kk < BK / 8; ++kk) {
+                            const uint64_t ah = smem_desc(a_base + kk * 32, 16, 1024);
+                            const uint64_t bh = smem_desc(b_base + kk * 32, 16, 1024);
+                            const uint64_t al = smem_desc(alo + kk * 32, 16, 1024);
+                            const uint64_t bl = smem_desc(blo + kk * 32, 16, 1024);
+                            tc_mma_tf32(dcol, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                            tc_mma_tf32(dcol, ah, bl, idesc, 1u);
+                            tc_mma_tf32(dcol, al, bh, idesc, 1u);
+                        }
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < BK / 8; ++kk) {
+                            // K-major: +32 B per 8 tf32 inside the 128-B swizzle row (SBO = 8 rows)
+                            // MN-major: +1024 B per 8 k-rows (LBO = stride of 32-wide MN chunks)
+                            const uint64_t ad = A_MN ? smem_desc(a_base + kk * 1024, GEMM_MN_LBO, GEMM_MN_SBO)
+                                                     : smem_desc(a_base + kk * 32, 16, 1024);
+                            const uint64_t bd = B_MN ? smem_desc(b_base + kk * 1024, GEMM_MN_LBO, GEMM_MN_SBO)
+                                                     : smem_desc(b_base + kk * 32, 16, 1024);
+                            tc_mma_tf32(dcol, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                        }
                     }
-                    tc_commit(&empty[s]);
-                    continue;
+                    tc_commit(&empty[s]);       // slot free once these MMAs have read it
                 }
-#pragma unroll
-                for (int kk = 0; kk < BK / 8; ++kk) {
-                    // K-major: +32 B per 8 tf32 inside the 128-B swizzle row (LBO unused, SBO = 8 rows)
-                    // MN-major: +1024 B per 8 k-rows (LBO = stride of 32-wide MN chunks, SBO = 8 rows)
-                    const uint64_t ad = A_MN ? smem_desc(a_base + kk * 1024, GEMM_MN_LBO, GEMM_MN_SBO)
-                                             : smem_desc(a_base + kk * 32, 16, 1024);
-                    const uint64_t bd = B_MN ? smem_desc(b_base + kk * 1024, GEMM_MN_LBO, GEMM_MN_SBO)
-                                             : smem_desc(b_base + kk * 32, 16, 1024);
-                    tc_mma_tf32(tmem, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
-                }
-                tc_commit(&empty[s]);       // slot free once these MMAs have read it
+                tc_commit(&tfull[acc]);         // accumulator complete
             }
-            tc_commit(tmem_full);           // accumulator complete
         }
-    } else {
+    } else if (warp < 6) {
         if (SPLIT3) {
-            // ---------------- converters: fp32 -> tf32 hi + lo (in place + lo buffer) ----------------
+            // ---------------- converters: fp32 -> tf32 hi (in place) + lo ----------------
             const int ct = threadIdx.x - 64;                 // 0..127
             constexpr int NV = C_::TMA_BYTES / 16;           // float4 per stage (A and B)
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % C_::STAGES;
-                const uint32_t ph = (uint32_t)(i / C_::STAGES) & 1u;
-                mbar_wait(&full[s], ph);
-                float4* base = reinterpret_cast<float4*>(stA(s));
-                float4* lo = reinterpret_cast<float4*>(stA(s) + C_::TMA_BYTES);
+            int it = 0;
+            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+                int m0, n0, kb0, nkb;
+                decode(t, m0, n0, kb0, nkb);
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % C_::STAGES;
+                    const uint32_t ph = (uint32_t)(it / C_::STAGES) & 1u;
+                    mbar_wait(&full[s], ph);
+                    float4* base = reinterpret_cast<float4*>(stA(s));
+                    float4* lo = reinterpret_cast<float4*>(stA(s) + C_::TMA_BYTES);
 #pragma unroll 4
-                for (int v = ct; v < NV; v += 128) {
-                    const float4 x = base[v];
-                    float4 h, l;
-                    h.x = tf32_rn(x.x); h.y = tf32_rn(x.y); h.z = tf32_rn(x.z); h.w = tf32_rn(x.w);
-                    l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
-                    base[v] = h;
-                    lo[v] = l;
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to tcgen05
-                __syncwarp();
-                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&conv[s])) : "memory");
-            }
-        }
-        // ---------------- epilogue: warps 2..5 ----------------
-        const int q = warp & 3;             // TMEM lane quarter this warp may access
-        const int row = m0 + 32 * q + lane;
-        if (nkb > 0) {
-            mbar_wait(tmem_full, 0);
-            tc_fence_after();
-        }
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-            float v[32];
-            if (nkb > 0) {
-                tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0, v);
-            } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = 0.f;
-            }
-            if (row >= M) continue;
-            const int col0 = n0 + c0;
-            if (ep.ws) {
-                float* w = ep.ws + ((int64_t)blockIdx.z * M + row) * ep.ldw;
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (col0 + j < ep.ldw) w[col0 + j] = (col0 + j < N) ? v[j] : 0.f;
-                continue;
-            }
-            float* crow = ep.C + (int64_t)row * ep.ldc;
-            const float* mrow = ep.mask ? ep.mask + (int64_t)row * ep.ldm : nullptr;
-            const bool full_chunk = (col0 + 32 <= N) && ((ep.ldc & 3) == 0) && !ep.accumulate;
-            if (full_chunk) {
-#pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                    float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                    if (mrow) {
-                        const float4 mk = *reinterpret_cast<const float4*>(mrow + col0 + j);
-                        if (!(mk.x > 0.f)) o.x = 0.f;
-                        if (!(mk.y > 0.f)) o.y = 0.f;
-                        if (!(mk.z > 0.f)) o.z = 0.f;
-                        if (!(mk.w > 0.f)) o.w = 0.f;
+                    for (int v = ct; v < NV; v += 128) {
+                        const float4 x = base[v];
+                        float4 h, l;
+                        h.x = tf32_rn(x.x); h.y = tf32_rn(x.y); h.z = tf32_rn(x.z); h.w = tf32_rn(x.w);
+                        l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+                        base[v] = h;
+                        lo[v] = l;
                     }
-                    *reinterpret_cast<float4*>(crow + col0 + j) = o;
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int col = col0 + j;
-                    if (col >= ep.ldc) break;
-                    float o = col < N ? v[j] : 0.f;
-                    if (mrow && col < N && !(mrow[col] > 0.f)) o = 0.f;
-                    if (ep.accumulate && col < N) o += crow[col];
-                    crow[col] = o;
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to tcgen05
+                    __syncwarp();
+                    if (lane == 0)
+                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&conv[s])) : "memory");
                 }
             }
+        }
+    } else {
+        // ---------------- epilogue: warps 6..9 ----------------
+        const int q = warp & 3;             // TMEM lane quarter this warp may access
+        int ti = 0;
+        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+            int m0, n0, kb0, nkb;
+            decode(t, m0, n0, kb0, nkb);
+            const int acc = ti & 1;
+            const uint32_t aph = (uint32_t)(ti >> 1) & 1u;
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            const int row = m0 + 32 * q + lane;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                float v[32];
+                tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c0), v);
+                if (row >= M) continue;
+                const int col0 = n0 + c0;
+                if (ep.ws) {
+                    float* w = ep.ws + ((int64_t)(t / (m_tiles * n_tiles)) * M + row) * ep.ldw;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (col0 + j < ep.ldw) w[col0 + j] = (col0 + j < N) ? v[j] : 0.f;
+                    continue;
+                }
+                float* crow = ep.C + (int64_t)row * ep.ldc;
+                const float* mrow = ep.mask ? ep.mask + (int64_t)row * ep.ldm : nullptr;
+                const bool full_chunk = (col0 + 32 <= N) && ((ep.ldc & 3) == 0) && !ep.accumulate;
+                if (full_chunk) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                        if (mrow) {
+                            const float4 mk = *reinterpret_cast<const float4*>(mrow + col0 + j);
+                            if (!(mk.x > 0.f)) o.x = 0.f;
+                            if (!(mk.y > 0.f)) o.y = 0.f;
+                            if (!(mk.z > 0.f)) o.z = 0.f;
+                            if (!(mk.w > 0.f)) o.w = 0.f;
+                        }
+                        *reinterpret_cast<float4*>(crow + col0 + j) = o;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int col = col0 + j;
+                        if (col >= ep.ldc) break;
+                        float o = col < N ? v[j] : 0.f;
+                        if (mrow && col < N && !(mrow[col] > 0.f)) o = 0.f;
+                        if (ep.accumulate && col < N) o += crow[col];
+                        crow[col] = o;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc])) : "memory");
         }
     }
     tc_fence_before();
@@ -428,9 +473,18 @@ int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, int64_t M, int6
     }
     const int total_kb = (int)((K + BK - 1) / BK);
     const int kbps = (total_kb + splits - 1) / splits;
-    const int zs = (total_kb + kbps - 1) / kbps;
-    dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), (unsigned)std::max(zs, 1));
-    kern<<<grid, kThreads, C_::SMEM, s>>>(ta, tb, (int)M, (int)N, total_kb, kbps, ep);
+    const int zs = std::max((total_kb + kbps - 1) / kbps, 1);
+    const int mt = (int)((M + BM - 1) / BM), nt = (int)((N + BN - 1) / BN);
+    const int64_t tiles = (int64_t)mt * nt * zs;
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+    kern<<<grid, kThreads, C_::SMEM, s>>>(ta, tb, (int)M, (int)N, total_kb, kbps, mt, nt, zs, ep);
     return cudaGetLastError() == cudaSuccess ? CDFGNN_OK : CDFGNN_ECUDA;
 }
 
