@@ -81,6 +81,8 @@ struct LocalPart {
     int32_t *rowptr = nullptr, *colidx = nullptr, *halo_local = nullptr;
     int32_t* order = nullptr;          // SpMM row order: degree-descending (longest first)
     float* xT = nullptr;               // cached H^(0)ᵀ (cfg.static_inputs) for ∇W^(0)
+    float* hT[CDFGNN_MAX_LAYERS] = {}; // H^(l)ᵀ written with the forward ReLU (epoch, tcgen05 path)
+    const float* hT_src[CDFGNN_MAX_LAYERS] = {};   // the H^(l) buffer hT[l] mirrors
     const float* xT_src = nullptr;     // the X pointer xT was built from
     float* val = nullptr;
     int64_t *moff_d = nullptr, *hoff_d = nullptr;
@@ -139,6 +141,7 @@ struct cdfgnn_ctx {
     size_t ws_bytes = 0;
     void* ws = nullptr;
     int transport = 0;                 // 0 co-resident (world 1), 1 NCCL send/recv, 2 NVLink push
+    bool in_epoch = false;             // Hᵀ reuse between forward and backward only inside cdfgnn_epoch
     std::vector<void*> peer_maps;      // IPC-opened peer allocations (push transport)
 };
 
@@ -279,6 +282,8 @@ void carve(cdfgnn_ctx* c, Bump& b) {
         c->trB = b.take<float>(c->Fmax * c->npad);
         if (c->cfg.static_inputs)
             for (LocalPart& P : c->parts) P.xT = b.take<float>((int64_t)c->cfg.dims[0] * ld_of(P.n));
+        for (LocalPart& P : c->parts)
+            for (int l = 1; l < c->cfg.L; ++l) P.hT[l] = b.take<float>((int64_t)c->cfg.dims[l] * ld_of(P.n));
     }
     c->stats_d = b.take<unsigned long long>(CDFGNN_MAX_LAYERS * 2 * 4);
     c->loss_d = b.take<double>(std::max(c->k, 1));
@@ -649,8 +654,15 @@ int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, cons
     if (H_out) {
         mark(c, PH_OTHER, s);
         for (int t = 0; t < c->k; ++t) {
-            launch_relu(Z[t], H_out[t], c->parts[t].n * ld_out, s);
-            c->launches++;
+            LocalPart& P = c->parts[t];
+            if (P.hT[l] && c->in_epoch) {
+                // ReLU fused with the transpose the next layer's ∇W needs (K-major Hᵀ)
+                c->launches += launch_relu_transpose(Z[t], P.n, Fo, ld_out, H_out[t], P.hT[l], ld_of(P.n), s);
+                P.hT_src[l] = H_out[t];
+            } else {
+                launch_relu(Z[t], H_out[t], P.n * ld_out, s);
+                c->launches++;
+            }
         }
         CDF_TRY(check_launch("relu"));
     }
@@ -679,6 +691,9 @@ int bwd_impl(cdfgnn_ctx* c, int l, float* const* dZ, int64_t ld, const float* co
                     P.xT_src = H_in[t];
                 }
                 Ht = P.xT;
+                ldh = ld_of(P.n);
+            } else if (l >= 2 && c->in_epoch && P.hT[l - 1] && P.hT_src[l - 1] == H_in[t]) {
+                Ht = P.hT[l - 1];               // written by the forward ReLU of layer l-1
                 ldh = ld_of(P.n);
             } else {
                 c->launches += launch_transpose(H_in[t], P.n, Fi, ld_in, c->trA, c->npad, s);
@@ -1080,7 +1095,10 @@ extern "C" int cdfgnn_epoch(cdfgnn_ctx* c, const float* const* X, const int32_t*
                             cdfgnn_epoch_stats* out, void* stream) {
     if (!c || !X || !labels || !train_mask || !W) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
     CUDA_TRY(cudaSetDevice(c->device));
-    return epoch_impl(c, X, labels, train_mask, W, out, (cudaStream_t)stream);
+    c->in_epoch = true;
+    const int rc = epoch_impl(c, X, labels, train_mask, W, out, (cudaStream_t)stream);
+    c->in_epoch = false;
+    return rc;
 }
 
 extern "C" int cdfgnn_epoch_host(cdfgnn_ctx* c, const float* const* X_host,
@@ -1101,7 +1119,10 @@ extern "C" int cdfgnn_epoch_host(cdfgnn_ctx* c, const float* const* X_host,
         CUDA_TRY(cudaMemcpyAsync(P.mask_stage, train_mask_host[t], P.n, cudaMemcpyHostToDevice, s));
         X[t] = P.X_stage; lab[t] = P.lab_stage; msk[t] = P.mask_stage;
     }
-    return epoch_impl(c, X.data(), lab.data(), msk.data(), W, out, s);
+    c->in_epoch = true;
+    const int rc = epoch_impl(c, X.data(), lab.data(), msk.data(), W, out, s);
+    c->in_epoch = false;
+    return rc;
 }
 
 extern "C" int cdfgnn_cache_view(cdfgnn_ctx* c, int32_t lp, int32_t l, int32_t dir, int32_t which,

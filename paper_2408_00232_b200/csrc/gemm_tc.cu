@@ -420,6 +420,27 @@ __global__ void transpose_kernel(const float* __restrict__ src, int64_t rows, in
     }
 }
 
+// H = max(Z, 0) row-major (rows x ldz, all ldz columns) and Hᵀ [cols x ldt] in one pass
+__global__ void relu_transpose_kernel(const float* __restrict__ Z, int64_t rows, int64_t cols, int64_t ldz,
+                                      float* __restrict__ H, float* __restrict__ Ht, int64_t ldt) {
+    __shared__ float tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        float v = 0.f;
+        if (r < rows && c < ldz) {
+            v = fmaxf(Z[r * ldz + c], 0.f);
+            H[r * ldz + c] = v;
+        }
+        tile[i][threadIdx.x] = v;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (c < cols && r < rows) Ht[c * ldt + r] = tile[threadIdx.x][i];
+    }
+}
+
 __global__ void pad_rows_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, float* __restrict__ dst,
                                 int64_t ldd) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -509,6 +530,14 @@ int launch_transpose(const float* src, int64_t rows, int64_t cols, int64_t lds, 
     if (rows <= 0 || cols <= 0) return 0;
     dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
     transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, lds, dst, ldd);
+    return 1;
+}
+
+int launch_relu_transpose(const float* Z, int64_t rows, int64_t cols, int64_t ldz, float* H, float* Ht,
+                          int64_t ldt, cudaStream_t s) {
+    if (rows <= 0) return 0;
+    dim3 grid((unsigned)((ldz + 31) / 32), (unsigned)((rows + 31) / 32));
+    relu_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(Z, rows, cols, ldz, H, Ht, ldt);
     return 1;
 }
 

@@ -106,6 +106,8 @@ void launch_gemm_simt(bool TA, bool TB, int64_t M, int64_t N, int64_t K, const f
                       bool accumulate, cudaStream_t s);
 // tcgen05 TF32 GEMMs (gemm_tc.cu); return a CDFGNN status
 int launch_pad_rows(const float* src, int64_t rows, int64_t cols, float* dst, int64_t ldd, cudaStream_t s);
+int launch_relu_transpose(const float* Z, int64_t rows, int64_t cols, int64_t ldz, float* H, float* Ht,
+                          int64_t ldt, cudaStream_t s);
 int launch_transpose(const float* src, int64_t rows, int64_t cols, int64_t lds, float* dst, int64_t ldd,
                      cudaStream_t s);
 // split3: 3xTF32 (A_hi·B_hi + A_hi·B_lo + A_lo·B_hi, ~fp32 accuracy); else 1xTF32 (RN inputs)

@@ -47,6 +47,27 @@ __device__ __forceinline__ float step8(float lo, float hi) {
     return __fmul_rn(__fsub_rn(hi, lo), 0.00390625f);   // RN((hi−lo)·2^-8)
 }
 
+// 4 consecutive uint8 codes at column c0 of an F-wide code row (one 32-bit access when the
+// row is 4-byte aligned, i.e. F % 4 == 0; out-of-range columns read as 0 / are not written)
+__device__ __forceinline__ void load_codes4(const uint8_t* row, int c0, int F, uint32_t (&q)[4]) {
+    if ((F & 3) == 0 && c0 + 3 < F) {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(row + c0);
+        q[0] = w & 0xFFu; q[1] = (w >> 8) & 0xFFu; q[2] = (w >> 16) & 0xFFu; q[3] = w >> 24;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q[k] = c0 + k < F ? row[c0 + k] : 0u;
+    }
+}
+__device__ __forceinline__ void store_codes4(uint8_t* row, int c0, int F, const uint32_t (&q)[4]) {
+    if ((F & 3) == 0 && c0 + 3 < F) {
+        *reinterpret_cast<uint32_t*>(row + c0) = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (c0 + k < F) row[c0 + k] = (uint8_t)q[k];
+    }
+}
+
 template <int LPR>
 __device__ __forceinline__ float gmax(float v) {
 #pragma unroll
@@ -193,13 +214,7 @@ __global__ void __launch_bounds__(kThreads) gather_pack_kernel(HaloDev h, SyncAr
                     const float sk = (c0 + k < a.F) ? __fadd_rn(comp(s4, k), dq8(q[k], lo[r], stp)) : 0.f;
                     setc(snew, k, sk);
                 }
-                if ((a.F & 3) == 0) {
-                    *reinterpret_cast<uint32_t*>(codes + c0) = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (c0 + k < a.F) codes[c0 + k] = (uint8_t)q[k];
-                }
+                store_codes4(codes, c0, a.F, q);
                 if (sr) st4(sr + c0, snew);     // reading R11: s ← s + deq(q(Δ))
             }
         } else {
@@ -274,10 +289,13 @@ __global__ void __launch_bounds__(kThreads) master_kernel(HaloDev h, SyncArgs a)
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
+                if (c0 >= a.F) continue;
+                uint32_t q[4];
+                load_codes4(codes, c0, a.F, q);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     if (c0 + k < a.F)
-                        setc(acc[v], k, __fadd_rn(comp(acc[v], k), dq8(codes[c0 + k], lo, stp)));
+                        setc(acc[v], k, __fadd_rn(comp(acc[v], k), dq8(q[k], lo, stp)));
             }
         } else {
             const float* prow = reinterpret_cast<const float*>(pay) + (int64_t)m * a.ld;
@@ -371,14 +389,14 @@ __global__ void __launch_bounds__(kThreads) master_kernel(HaloDev h, SyncArgs a)
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
+                if (c0 >= a.F) continue;
+                uint32_t q[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    if (c0 + k < a.F) {
-                        const uint32_t qk = q8(comp(del[v], k), lo, rng);
-                        codes[c0 + k] = (uint8_t)qk;
-                        setc(b[v], k, __fadd_rn(comp(b[v], k), dq8(qk, lo, stp)));
-                    }
+                    q[k] = q8(comp(del[v], k), lo, rng);
+                    if (c0 + k < a.F) setc(b[v], k, __fadd_rn(comp(b[v], k), dq8(q[k], lo, stp)));
                 }
+                store_codes4(codes, c0, a.F, q);
             }
         } else {
 #pragma unroll
@@ -535,10 +553,13 @@ __global__ void __launch_bounds__(kThreads) mirror_apply_kernel(HaloDev h, SyncA
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
+                if (c0 >= a.F) continue;
+                uint32_t q[4];
+                load_codes4(codes, c0, a.F, q);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     if (c0 + k < a.F)
-                        setc(b[v], k, __fadd_rn(comp(b[v], k), dq8(codes[c0 + k], lo, stp)));
+                        setc(b[v], k, __fadd_rn(comp(b[v], k), dq8(q[k], lo, stp)));
             }
         } else {
             const float* prow = reinterpret_cast<const float*>(pay) + (int64_t)m * a.ld;
