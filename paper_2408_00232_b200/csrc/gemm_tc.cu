@@ -30,7 +30,10 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;            // 32 tf32 = 128 bytes: one swizzle row
-constexpr int kThreads = 320;     // 10 warps: TMA, MMA, 4 x converter, 4 x epilogue
+constexpr int kConvWarps = 4;     // 3xTF32 converter warps
+constexpr int kEpiWarps = 8;      // two epilogue warpgroups split each tile's column chunks
+constexpr int kEpiWarp0 = 2 + kConvWarps;
+constexpr int kThreads = 32 * (2 + kConvWarps + kEpiWarps);   // TMA, MMA, converters, epilogue
 #ifndef GEMM_MN_LBO
 #define GEMM_MN_LBO (BK * 128)   // MN-major: byte stride between 32-element MN chunks
 #endif
@@ -125,7 +128,8 @@ struct Cfg {
     static constexpr int TMA_BYTES = A_BYTES + B_BYTES;                  // fp32 (or tf32) tiles
     static constexpr int STAGE_BYTES = TMA_BYTES * (SPLIT3 ? 2 : 1);     // + lo parts for 3xTF32
     static constexpr int STAGES = (SPLIT3 ? 196608 : 200704) / STAGE_BYTES;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int EPI_BYTES = kEpiWarps * 32 * 33 * 4;            // epilogue transpose staging
+    static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;        // double-buffered accumulator
 };
 
@@ -162,7 +166,8 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     // stage s: [A (hi)][B (hi)][A lo][B lo]   (lo parts only with SPLIT3)
     auto stA = [&](int st) { return smem + st * C_::STAGE_BYTES; };
     auto stB = [&](int st) { return smem + st * C_::STAGE_BYTES + C_::A_BYTES; };
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C_::STAGES * C_::STAGE_BYTES);
+    float* epi_smem = reinterpret_cast<float*>(smem + C_::STAGES * C_::STAGE_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C_::STAGES * C_::STAGE_BYTES + C_::EPI_BYTES);
     uint64_t* empty = full + C_::STAGES;
     uint64_t* conv = empty + C_::STAGES;
     uint64_t* tfull = conv + C_::STAGES;      // [2] accumulator ready
@@ -176,11 +181,11 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         for (int s = 0; s < C_::STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
-            mbar_init(&conv[s], 4);          // one arrival per converter warp
+            mbar_init(&conv[s], kConvWarps);   // one arrival per converter warp
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);        // one arrival per epilogue warp
+            mbar_init(&tempty[a], kEpiWarps);   // one arrival per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -293,10 +298,10 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 tc_commit(&tfull[acc]);         // accumulator complete
             }
         }
-    } else if (warp < 6) {
+    } else if (warp < kEpiWarp0) {
         if (SPLIT3) {
             // ---------------- converters: fp32 -> tf32 hi (in place) + lo ----------------
-            const int ct = threadIdx.x - 64;                 // 0..127
+            const int ct = threadIdx.x - 64;                 // 0 .. 32*kConvWarps-1
             constexpr int NV = C_::TMA_BYTES / 16;           // float4 per stage (A and B)
             int it = 0;
             for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
@@ -309,7 +314,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     float4* base = reinterpret_cast<float4*>(stA(s));
                     float4* lo = reinterpret_cast<float4*>(stA(s) + C_::TMA_BYTES);
 #pragma unroll 4
-                    for (int v = ct; v < NV; v += 128) {
+                    for (int v = ct; v < NV; v += 32 * kConvWarps) {
                         const float4 x = base[v];
                         float4 h, l;
                         h.x = tf32_rn(x.x); h.y = tf32_rn(x.y); h.z = tf32_rn(x.z); h.w = tf32_rn(x.w);
@@ -325,8 +330,9 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             }
         }
     } else {
-        // ---------------- epilogue: warps 6..9 ----------------
+        // ---------------- epilogue warps ----------------
         const int q = warp & 3;             // TMEM lane quarter this warp may access
+        const int eg = (warp - kEpiWarp0) >> 2;   // epilogue warpgroup: even / odd 32-column chunks
         int ti = 0;
         for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
             int m0, n0, kb0, nkb;
@@ -335,45 +341,71 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             const uint32_t aph = (uint32_t)(ti >> 1) & 1u;
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
-            const int row = m0 + 32 * q + lane;
+            // each lane holds one accumulator row; 32x32 chunks are transposed through shared
+            // memory so every global store instruction writes 4 full 128-byte row segments
+            float* st = epi_smem + (warp - kEpiWarp0) * 32 * 33;
+            const int rbase = m0 + 32 * q;
+            const bool vec = (ep.ws ? (ep.ldw & 3) == 0 : (ep.ldc & 3) == 0) &&
+                             (!ep.mask || (ep.ldm & 3) == 0);
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
+            for (int c0 = 32 * eg; c0 < BN; c0 += 64) {
                 float v[32];
                 tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c0), v);
-                if (row >= M) continue;
                 const int col0 = n0 + c0;
-                if (ep.ws) {
-                    float* w = ep.ws + ((int64_t)(t / (m_tiles * n_tiles)) * M + row) * ep.ldw;
+                const int64_t ldo = ep.ws ? ep.ldw : ep.ldc;
+                if (col0 >= ldo) continue;                     // warp-uniform
+                float* obase = ep.ws ? ep.ws + (int64_t)(t / (m_tiles * n_tiles)) * M * ep.ldw : ep.C;
+                if (vec) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (col0 + j < ep.ldw) w[col0 + j] = (col0 + j < N) ? v[j] : 0.f;
-                    continue;
-                }
-                float* crow = ep.C + (int64_t)row * ep.ldc;
-                const float* mrow = ep.mask ? ep.mask + (int64_t)row * ep.ldm : nullptr;
-                const bool full_chunk = (col0 + 32 <= N) && ((ep.ldc & 3) == 0) && !ep.accumulate;
-                if (full_chunk) {
+                    for (int j = 0; j < 32; ++j) st[lane * 33 + j] = v[j];
+                    __syncwarp();
+                    const int rr = lane >> 3, cc = (lane & 7) * 4;
+                    const int col = col0 + cc;
+                    // masks (and accumulate inputs) for all 8 row groups in flight together
+                    float4 mk[8], ci[8];
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                        if (mrow) {
-                            const float4 mk = *reinterpret_cast<const float4*>(mrow + col0 + j);
-                            if (!(mk.x > 0.f)) o.x = 0.f;
-                            if (!(mk.y > 0.f)) o.y = 0.f;
-                            if (!(mk.z > 0.f)) o.z = 0.f;
-                            if (!(mk.w > 0.f)) o.w = 0.f;
-                        }
-                        *reinterpret_cast<float4*>(crow + col0 + j) = o;
+                    for (int g = 0; g < 8; ++g) {
+                        const int row = rbase + 4 * g + rr;
+                        const bool ok = row < M && col < ldo;
+                        mk[g] = (ep.mask && ok) ? *reinterpret_cast<const float4*>(ep.mask + (int64_t)row * ep.ldm + col)
+                                                : make_float4(1.f, 1.f, 1.f, 1.f);
+                        ci[g] = (ep.accumulate && !ep.ws && ok)
+                                    ? *reinterpret_cast<const float4*>(obase + (int64_t)row * ldo + col)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
-                } else {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int col = col0 + j;
-                        if (col >= ep.ldc) break;
-                        float o = col < N ? v[j] : 0.f;
-                        if (mrow && col < N && !(mrow[col] > 0.f)) o = 0.f;
-                        if (ep.accumulate && col < N) o += crow[col];
-                        crow[col] = o;
+                    for (int g = 0; g < 8; ++g) {
+                        const int i = 4 * g;
+                        const int row = rbase + i + rr;
+                        if (row < M && col < ldo) {
+                            float4 o;
+                            o.x = col + 0 < N ? st[(i + rr) * 33 + cc + 0] : 0.f;
+                            o.y = col + 1 < N ? st[(i + rr) * 33 + cc + 1] : 0.f;
+                            o.z = col + 2 < N ? st[(i + rr) * 33 + cc + 2] : 0.f;
+                            o.w = col + 3 < N ? st[(i + rr) * 33 + cc + 3] : 0.f;
+                            if (!(mk[g].x > 0.f)) o.x = 0.f;
+                            if (!(mk[g].y > 0.f)) o.y = 0.f;
+                            if (!(mk[g].z > 0.f)) o.z = 0.f;
+                            if (!(mk[g].w > 0.f)) o.w = 0.f;
+                            o.x += ci[g].x; o.y += ci[g].y; o.z += ci[g].z; o.w += ci[g].w;
+                            *reinterpret_cast<float4*>(obase + (int64_t)row * ldo + col) = o;
+                        }
+                    }
+                    __syncwarp();
+                } else {
+                    const int row = rbase + lane;
+                    if (row < M) {
+                        float* orow = obase + (int64_t)row * ldo;
+                        const float* mrow = ep.mask ? ep.mask + (int64_t)row * ep.ldm : nullptr;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const int col = col0 + j;
+                            if (col >= ldo) break;
+                            float o = col < N ? v[j] : 0.f;
+                            if (mrow && col < N && !(mrow[col] > 0.f)) o = 0.f;
+                            if (ep.accumulate && !ep.ws && col < N) o += orow[col];
+                            orow[col] = o;
+                        }
                     }
                 }
             }
