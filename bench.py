@@ -38,6 +38,8 @@ def parse():
                     choices=["cache_int8", "cache_fp32", "quant_only", "nocache"])
     ap.add_argument("--eps0", type=float, default=0.01)
     ap.add_argument("--transport", default="push", choices=["push", "nccl"])
+    ap.add_argument("--overlap", action="store_true",
+                    help="boundary-rows-first scheduling (gather phase on a second stream; off by default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-frac", type=float, default=0.01)
@@ -221,7 +223,8 @@ def main(args):
             "nocache": (False, 0)}[args.mode]
     run = Run(ds, world, rank=rank, world=world, device=local, cache=mode[0], quant_bits=mode[1],
               eps0=args.eps0, adaptive=True, optimizer="adam", lr=0.01, timing=True,
-              host_inputs=not args.no_e2e, transport=args.transport, static_inputs=True)
+              host_inputs=not args.no_e2e, transport=args.transport, static_inputs=True,
+              overlap=args.overlap)
     t_prep = time.time() - t_prep
     for _ in range(args.warmup):
         run.epoch()
@@ -324,6 +327,7 @@ def main(args):
                                f"dims {'-'.join(map(str, cfgc.dims))}",
                    "mode": args.mode, "partitions": world, "parallelism": f"vertex-cut p{world}",
                    "transport": ["none", "nccl", "nvlink-push"][stats[-1]["transport"]],
+                   "overlap": args.overlap and world > 1 and stats[-1]["transport"] != 1,
                    "l2": "inputs larger than L2 (CSR %.2f GB, X %.2f GB)" %
                          (2 * ds.m * 8 / 1e9, ds.X.nbytes / 1e9)},
         "comm_bytes_per_epoch": int(tot[0]), "comm_wire_bytes_per_epoch": int(tot[1]),

@@ -156,6 +156,16 @@ typedef struct {
     int32_t static_inputs;              /* 1: the input features X do not change between calls for
                                            a given buffer, so Xᵀ (∇W^(0) operand) is built once per
                                            X pointer and reused; 0 (default): rebuilt every epoch */
+    int32_t overlap;                    /* 1: boundary-rows-first scheduling (§8 f1) — the SpMM
+                                           (forward) or ∇H GEMM (backward, inside cdfgnn_epoch)
+                                           produces the mirror rows first, their gather phase (test,
+                                           pack, NVLink push, barrier) runs on a second, high-priority
+                                           stream while the master and interior rows are computed.
+                                           Bitwise-identical results; used when p > 1 and the
+                                           transport has no host round trip (push or co-resident).
+                                           0 (default): measured slower on B200 — the
+                                           split SpMM and the concurrent streaming kernels cost more
+                                           L2 bandwidth than the hidden gather saves */
 } cdfgnn_cfg;
 
 int cdfgnn_cfg_default(cdfgnn_cfg* cfg);

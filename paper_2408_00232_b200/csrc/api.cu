@@ -68,6 +68,18 @@ enum Phase { PH_GEMM = 0, PH_SPMM = 1, PH_SYNC = 2, PH_OTHER = 3, PH_END = 4 };
 // sub-phases of the halo exchange (tag of PH_SYNC marks)
 enum SyncSub { SS_GPACK = 0, SS_GXFER = 1, SS_MASTER = 2, SS_SPACK = 3, SS_SXFER = 4, SS_MIRROR = 5 };
 
+// SpMM work-item schedule of one part for one row-width class (kernels_spmm.cu)
+struct SpmmPlan {
+    std::vector<int2> items_h, items2_h;   // all rows | [mirror rows][master + interior rows]
+    std::vector<int4> split_h;             // per row {partial slot, segments, seg_beg index}
+    std::vector<int32_t> seg_beg_h;
+    int64_t n_items = 0, n_items_mir = 0, nslots = 0, pstride = 0;
+    int2 *items = nullptr, *items2 = nullptr;
+    int4* split = nullptr;
+    int32_t *seg_beg = nullptr, *pcounter = nullptr;
+    float* partial = nullptr;
+};
+
 struct LocalPart {
     int32_t part = 0;
     int64_t n = 0, B = 0, M = 0, nnz = 0;
@@ -79,7 +91,7 @@ struct LocalPart {
     std::vector<int64_t> capA, capB;   // region capacities per peer
     // device
     int32_t *rowptr = nullptr, *colidx = nullptr, *halo_local = nullptr;
-    int32_t* order = nullptr;          // SpMM row order: degree-descending (longest first)
+    SpmmPlan sp[2];                    // SpMM work items: [0] wide rows (ld > 64), [1] narrow rows
     float* xT = nullptr;               // cached H^(0)ᵀ (cfg.static_inputs) for ∇W^(0)
     float* hT[CDFGNN_MAX_LAYERS] = {}; // H^(l)ᵀ written with the forward ReLU (epoch, tcgen05 path)
     const float* hT_src[CDFGNN_MAX_LAYERS] = {};   // the H^(l) buffer hT[l] mirrors
@@ -143,11 +155,108 @@ struct cdfgnn_ctx {
     int transport = 0;                 // 0 co-resident (world 1), 1 NCCL send/recv, 2 NVLink push
     bool in_epoch = false;             // Hᵀ reuse between forward and backward only inside cdfgnn_epoch
     std::vector<void*> peer_maps;      // IPC-opened peer allocations (push transport)
+    // boundary-rows-first overlap (cfg.overlap): gather phases run on s2
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t evA = nullptr, evB = nullptr;
+    bool pend[CDFGNN_MAX_LAYERS][2] = {};   // gather of (l, dir) already launched on s2
 };
 
 namespace {
 
 int64_t sync_width(const cdfgnn_ctx* c, int l) { return c->cfg.dims[l]; }
+
+// SpMM work items of a part (kernels_spmm.cu).  phases > 1: rows with more than
+// `min_deg` neighbours are split by column range into `phases` segments, visited
+// phase-major (each segment list longest first), then the unsplit rows longest first.
+// Else chunk > 0: rows longer than `chunk` neighbours become ceil(deg/chunk) chunks and
+// every item is visited longest first.  items2_h holds the same items with the mirror
+// rows' first (boundary-rows-first scheduling, §8 f1), order otherwise kept.
+void build_spmm_items(const LocalPart& P, SpmmPlan& S, int chunk, int phases, int min_deg) {
+    S.split_h.assign(P.n, make_int4(-1, 0, 0, 0));
+    S.seg_beg_h.clear();
+    S.nslots = 0;
+    std::vector<std::pair<int32_t, int2>> w;      // (weight, item)
+    std::vector<std::pair<int32_t, int2>> tail;   // unsplit rows (phase mode)
+    w.reserve(P.n);
+    auto split_row = [&](int64_t r, const std::vector<int32_t>& starts) {
+        const int nseg = (int)starts.size() - 1;
+        S.split_h[r] = make_int4((int)S.nslots, nseg, (int)S.seg_beg_h.size(), 0);
+        S.nslots += nseg;
+        S.seg_beg_h.insert(S.seg_beg_h.end(), starts.begin(), starts.end());
+    };
+    if (phases > 1) {
+        std::vector<std::vector<std::pair<int32_t, int2>>> ph(phases);
+        std::vector<int32_t> st(phases + 1);
+        for (int64_t r = 0; r < P.n; ++r) {
+            const int32_t rb = P.rowptr_h[r], re = P.rowptr_h[r + 1];
+            if (re - rb <= min_deg) {
+                tail.push_back({re - rb, make_int2((int)r, -1)});
+                continue;
+            }
+            st[0] = rb;
+            st[phases] = re;
+            for (int k = 1; k < phases; ++k) {
+                const int32_t bound = (int32_t)((int64_t)k * P.n / phases);
+                st[k] = (int32_t)(std::lower_bound(P.colidx_h + rb, P.colidx_h + re, bound) - P.colidx_h);
+            }
+            split_row(r, st);
+            for (int k = 0; k < phases; ++k) ph[k].push_back({st[k + 1] - st[k], make_int2((int)r, k)});
+        }
+        auto by_weight = [](const std::pair<int32_t, int2>& a, const std::pair<int32_t, int2>& b) {
+            return a.first > b.first;
+        };
+        for (auto& v : ph) {
+            std::stable_sort(v.begin(), v.end(), by_weight);
+            w.insert(w.end(), v.begin(), v.end());
+        }
+        std::stable_sort(tail.begin(), tail.end(), by_weight);
+        w.insert(w.end(), tail.begin(), tail.end());
+    } else {
+        std::vector<int32_t> st;
+        for (int64_t r = 0; r < P.n; ++r) {
+            const int32_t rb = P.rowptr_h[r], re = P.rowptr_h[r + 1], deg = re - rb;
+            if (chunk > 0 && deg > chunk) {
+                const int32_t nch = (deg + chunk - 1) / chunk;
+                st.resize(nch + 1);
+                for (int32_t ch = 0; ch < nch; ++ch) st[ch] = rb + ch * chunk;
+                st[nch] = re;
+                split_row(r, st);
+                for (int32_t ch = 0; ch < nch; ++ch)
+                    w.push_back({std::min(chunk, deg - ch * chunk), make_int2((int)r, ch)});
+            } else {
+                w.push_back({deg, make_int2((int)r, -1)});
+            }
+        }
+        std::stable_sort(w.begin(), w.end(), [](const std::pair<int32_t, int2>& a, const std::pair<int32_t, int2>& b) {
+            return a.first > b.first;
+        });
+    }
+    if (S.seg_beg_h.empty()) S.seg_beg_h.push_back(0);
+    S.n_items = (int64_t)w.size();
+    S.items_h.resize(w.size());
+    for (size_t i = 0; i < w.size(); ++i) S.items_h[i] = w[i].second;
+    S.items2_h.clear();
+    S.items2_h.reserve(w.size());
+    auto is_mirror = [&](const int2& it) { return it.x >= P.B && it.x < P.B + P.M; };
+    for (const int2& it : S.items_h)
+        if (is_mirror(it)) S.items2_h.push_back(it);
+    S.n_items_mir = (int64_t)S.items2_h.size();
+    for (const int2& it : S.items_h)
+        if (!is_mirror(it)) S.items2_h.push_back(it);
+}
+
+SpmmPlan& spmm_plan(LocalPart& P, int64_t ld) { return P.sp[ld <= 64 ? 1 : 0]; }
+
+SpmmItems spmm_items(LocalPart& P, int rows, int64_t ld) {
+    const SpmmPlan& S = spmm_plan(P, ld);
+    SpmmItems it;
+    it.items = rows == 0 ? S.items : (rows == 1 ? S.items2 : S.items2 + S.n_items_mir);
+    it.split = S.split;
+    it.seg_beg = S.seg_beg;
+    it.partial = S.partial;
+    it.counter = S.pcounter;
+    return it;
+}
 
 // host-side sizes from the plan
 int prepare(cdfgnn_ctx* c, const cdfgnn_plan* plan, const int32_t* parts, int32_t k,
@@ -205,6 +314,12 @@ int prepare(cdfgnn_ctx* c, const cdfgnn_plan* plan, const int32_t* parts, int32_
             P.capA[j] = P.moff[j + 1] - P.moff[j];
             P.capB[j] = P.hoff[j + 1] - P.hoff[j];
         }
+        // wide rows: LPT over whole rows (chunks cost L2 bandwidth there, profiles/r1);
+        // narrow rows: hub rows split into chunks (their latency chains dominated)
+        build_spmm_items(P, P.sp[0], spmm_chunk(true), spmm_default_phases(), spmm_phase_min_degree());
+        build_spmm_items(P, P.sp[1], spmm_chunk(false), spmm_default_phases(), spmm_phase_min_degree());
+        P.sp[0].pstride = c->ldmax;
+        P.sp[1].pstride = std::min<int64_t>(c->ldmax, 64);
     }
     return CDFGNN_OK;
 }
@@ -219,7 +334,14 @@ void carve(cdfgnn_ctx* c, Bump& b) {
     for (LocalPart& P : c->parts) {
         P.rowptr = b.take<int32_t>(P.n + 1);
         P.colidx = b.take<int32_t>(P.nnz);
-        P.order = b.take<int32_t>(P.n);
+        for (SpmmPlan& S : P.sp) {
+            S.items = b.take<int2>(S.n_items);
+            S.items2 = b.take<int2>(S.n_items);
+            S.split = b.take<int4>(P.n);
+            S.seg_beg = b.take<int32_t>((int64_t)S.seg_beg_h.size());
+            S.pcounter = b.take<int32_t>(S.nslots);
+            S.partial = b.take<float>(S.nslots * S.pstride);
+        }
         P.val = b.take<float>(P.nnz);
         P.halo_local = b.take<int32_t>(P.hoff[p]);
         P.moff_d = b.take<int64_t>(p + 1);
@@ -512,16 +634,10 @@ int setup_push(cdfgnn_ctx* c, cudaStream_t s) {
     return CDFGNN_OK;
 }
 
-// skip_gather / skip_scatter: §8 f2 dead-sync elision inside cdfgnn_epoch — the layer-L
-// forward scatter (mirrors never read logits, the loss is on masters, P:L256) and the
-// layer-L backward gather (mirrors' δ̈^(L) is identically zero) carry no information.
-int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float eps,
-              cudaStream_t s, int64_t* wire, bool skip_gather = false, bool skip_scatter = false) {
-    const int p = c->p;
+void sync_args(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float eps, bool skip_gather,
+               std::vector<SyncArgs>& args) {
     const int F = (int)sync_width(c, l);
-    if (ld != ld_of(F)) CDF_FAIL(CDFGNN_EUSAGE, "ld %lld must equal roundup(F=%d, 4)", (long long)ld, F);
-    mark(c, PH_SYNC, s, SS_GPACK);
-    std::vector<SyncArgs> args(c->k);
+    args.assign(c->k, SyncArgs{});
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
         SyncArgs& a = args[t];
@@ -531,24 +647,45 @@ int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float 
         a.stats = c->stats_d + ((l - 1) * 2 + dir) * 4;
         a.no_msgs = skip_gather ? 1 : 0;
     }
+}
+
+// Gather phase of one synchronisation (Alg. 2 L3-L9): mirrors test, quantise, pack, and the
+// transfer to the master parts.  Runs on `s` (the caller stream, or c->s2 when overlapped).
+int halo_gather(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float eps,
+                cudaStream_t s, int64_t* wire) {
+    const int p = c->p;
+    const int F = (int)sync_width(c, l);
+    if (ld != ld_of(F)) CDF_FAIL(CDFGNN_EUSAGE, "ld %lld must equal roundup(F=%d, 4)", (long long)ld, F);
+    std::vector<SyncArgs> args;
+    sync_args(c, l, dir, X, ld, eps, false, args);
     const int64_t rowb = c->cfg.quant_bits ? F : 4 * ld;
-    // ---- gather: mirrors test, quantise, pack (Alg. 2 L3-L9)
-    for (int t = 0; t < c->k && !skip_gather; ++t) {
+    for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
         const int nt = gather_tiles_host(P.moff.data(), p, ld);
         CUDA_TRY(cudaMemsetAsync(P.cnt, 0, sizeof(int32_t) * p, s));       // range reservations
         c->launches += launch_gather_pack_n(P.halo, args[t], nt, s);
     }
     CDF_TRY(check_launch("gather_pack"));
-    mark(c, PH_SYNC, s, SS_GXFER);
-    if (c->transport == 1 && !skip_gather) CDF_TRY(nccl_phase(c, c->parts[0], true, rowb, s, wire));
-    if (c->transport == 2 && !skip_gather) {
+    if (!(c->s2 && s == c->s2)) mark(c, PH_SYNC, s, SS_GXFER);   // no marks on the side stream
+    if (c->transport == 1) CDF_TRY(nccl_phase(c, c->parts[0], true, rowb, s, wire));
+    if (c->transport == 2) {
         LocalPart& P = c->parts[0];
         c->launches += launch_put(P.putG_d, p, c->hdr_bytes, rowb,
                                   *std::max_element(P.capA.begin(), P.capA.end()), s);
         CDF_TRY(check_launch("put gather"));
         CDF_TRY(push_barrier(c, s));
     }
+    return CDFGNN_OK;
+}
+
+// Master apply + scatter phase (Alg. 2 L10-L22).  skip_gather: no gather ran (§8 f2).
+int halo_finish(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float eps,
+                cudaStream_t s, int64_t* wire, bool skip_gather, bool skip_scatter) {
+    const int p = c->p;
+    const int F = (int)sync_width(c, l);
+    std::vector<SyncArgs> args;
+    sync_args(c, l, dir, X, ld, eps, skip_gather, args);
+    const int64_t rowb = c->cfg.quant_bits ? F : 4 * ld;
     mark(c, PH_SYNC, s, SS_MASTER);
     // ---- masters: apply in ascending source order, own test, stage scatter (L10-L19)
     for (int t = 0; t < c->k; ++t) {
@@ -592,6 +729,45 @@ int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float 
     return CDFGNN_OK;
 }
 
+// skip_gather / skip_scatter: §8 f2 dead-sync elision inside cdfgnn_epoch — the layer-L
+// forward scatter (mirrors never read logits, the loss is on masters, P:L256) and the
+// layer-L backward gather (mirrors' δ̈^(L) is identically zero) carry no information.
+int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float eps,
+              cudaStream_t s, int64_t* wire, bool skip_gather = false, bool skip_scatter = false) {
+    const int F = (int)sync_width(c, l);
+    if (ld != ld_of(F)) CDF_FAIL(CDFGNN_EUSAGE, "ld %lld must equal roundup(F=%d, 4)", (long long)ld, F);
+    mark(c, PH_SYNC, s, SS_GPACK);
+    if (!skip_gather) CDF_TRY(halo_gather(c, l, dir, X, ld, eps, s, wire));
+    else mark(c, PH_SYNC, s, SS_GXFER);
+    return halo_finish(c, l, dir, X, ld, eps, s, wire, skip_gather, skip_scatter);
+}
+
+// The overlapped schedule applies when there is something to exchange and the transfer has no
+// host round trip (NVLink push, or co-resident parts); the NCCL transport reads counts on the host.
+bool overlap_on(const cdfgnn_ctx* c) { return c->cfg.overlap && c->p > 1 && c->transport != 1 && c->s2; }
+
+// Hand the gather of (l, dir) to s2 once the caller stream has produced every mirror row.
+int launch_gather_async(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float eps,
+                        cudaStream_t s, int64_t* wire) {
+    static const bool serial = getenv("CDFGNN_OVL_SERIAL") && atoi(getenv("CDFGNN_OVL_SERIAL"));
+    cudaStream_t gs = serial ? s : c->s2;
+    CUDA_TRY(cudaEventRecord(c->evA, s));
+    CUDA_TRY(cudaStreamWaitEvent(gs, c->evA, 0));
+    CDF_TRY(halo_gather(c, l, dir, X, ld, eps, gs, wire));
+    CUDA_TRY(cudaEventRecord(c->evB, gs));
+    c->pend[l - 1][dir] = true;
+    return CDFGNN_OK;
+}
+
+// Join a gather launched by launch_gather_async, then finish the synchronisation on s.
+int halo_join_finish(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float eps,
+                     cudaStream_t s, int64_t* wire, bool skip_scatter) {
+    mark(c, PH_SYNC, s, SS_GXFER);          // exposed (not hidden) part of the gather phase
+    CUDA_TRY(cudaStreamWaitEvent(s, c->evB, 0));
+    c->pend[l - 1][dir] = false;
+    return halo_finish(c, l, dir, X, ld, eps, s, wire, false, skip_scatter);
+}
+
 void fill_sync_stats(const cdfgnn_ctx* c, int l, int dir, const unsigned long long* h, int64_t wire,
                      cdfgnn_sync_stats* st) {
     const int64_t F = sync_width(c, l);
@@ -619,9 +795,14 @@ int read_stats_now(cdfgnn_ctx* c, int l, int dir, int64_t wire, cudaStream_t s,
     return CDFGNN_OK;
 }
 
-int spmm_part(cdfgnn_ctx* c, LocalPart& P, const float* T, float* Y, int64_t ld, cudaStream_t s) {
+// rows: 0 = all rows (longest first), 1 = mirror rows only, 2 = master + interior rows only
+int spmm_part(cdfgnn_ctx* c, LocalPart& P, const float* T, float* Y, int64_t ld, cudaStream_t s,
+              int rows = 0) {
+    const SpmmPlan& S = spmm_plan(P, ld);
+    const int64_t n = rows == 0 ? S.n_items : (rows == 1 ? S.n_items_mir : S.n_items - S.n_items_mir);
+    if (n <= 0) return CDFGNN_OK;
     mark(c, PH_SPMM, s, ld);
-    launch_spmm(P.rowptr, P.colidx, P.val, P.n, T, Y, ld, P.order, s);
+    launch_spmm(P.rowptr, P.colidx, P.val, n, spmm_items(P, rows, ld), T, Y, ld, s);
     c->launches++;
     return check_launch("spmm");
 }
@@ -633,6 +814,7 @@ int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, cons
     if (ld_in < Fi || ld_in % 4 || ld_out != ld_of(Fo)) CDF_FAIL(CDFGNN_EUSAGE, "bad leading dimension");
     float* Wt = c->wtpad + c->wtoff[l - 1];
     const int64_t ldwt = ld_of(Fi);
+    const bool ov = overlap_on(c);
     if (c->cfg.gemm_tf32) {
         mark(c, PH_GEMM, s);
         c->launches += launch_transpose(W, Fi, Fo, Fo, Wt, ldwt, s);
@@ -648,9 +830,16 @@ int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, cons
         }
         c->launches++;
         CDF_TRY(check_launch("gemm fwd"));
-        CDF_TRY(spmm_part(c, P, P.T, Z[t], ld_out, s));
+        CDF_TRY(spmm_part(c, P, P.T, Z[t], ld_out, s, ov ? 1 : 0));
     }
-    CDF_TRY(halo_impl(c, l, 0, Z, ld_out, eps, s, wire, false, elide && l == c->cfg.L));
+    if (ov) {
+        // §8 f1: the mirror rows are done — their gather runs on s2 under the remaining SpMM rows
+        CDF_TRY(launch_gather_async(c, l, 0, Z, ld_out, eps, s, wire));
+        for (int t = 0; t < c->k; ++t) CDF_TRY(spmm_part(c, c->parts[t], c->parts[t].T, Z[t], ld_out, s, 2));
+        CDF_TRY(halo_join_finish(c, l, 0, Z, ld_out, eps, s, wire, elide && l == c->cfg.L));
+    } else {
+        CDF_TRY(halo_impl(c, l, 0, Z, ld_out, eps, s, wire, false, elide && l == c->cfg.L));
+    }
     if (H_out) {
         mark(c, PH_OTHER, s);
         for (int t = 0; t < c->k; ++t) {
@@ -669,19 +858,46 @@ int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, cons
     return CDFGNN_OK;
 }
 
+// wire_prev: transfer counter of the (l-1, δ) sync, whose gather this call may launch early
 int bwd_impl(cdfgnn_ctx* c, int l, float* const* dZ, int64_t ld, const float* const* H_in,
              int64_t ld_in, const float* W, float* const* dZ_prev, float* dW, float eps,
-             cudaStream_t s, int64_t* wire, bool elide = false) {
+             cudaStream_t s, int64_t* wire, bool elide = false, int64_t* wire_prev = nullptr) {
     const int64_t Fi = c->cfg.dims[l - 1], Fo = c->cfg.dims[l];
     if (ld != ld_of(Fo) || ld_in < Fi || ld_in % 4) CDF_FAIL(CDFGNN_EUSAGE, "bad leading dimension");
-    CDF_TRY(halo_impl(c, l, 1, dZ, ld, eps, s, wire, elide && l == c->cfg.L, false));
+    if (c->pend[l - 1][1]) CDF_TRY(halo_join_finish(c, l, 1, dZ, ld, eps, s, wire, false));
+    else CDF_TRY(halo_impl(c, l, 1, dZ, ld, eps, s, wire, elide && l == c->cfg.L, false));
+    // §8 f1 in the backward pass: δ̈^(l-1) mirror rows first, their gather on s2 under ∇W and
+    // the remaining rows (inside cdfgnn_epoch, where the next call joins it)
+    const bool ov = dZ_prev && c->in_epoch && overlap_on(c) && ld_in == ld_of(Fi);
+    // δ̈^(l-1) rows [r0, r1) of part t: (S Wᵀ) ⊙ 𝟙[H > 0]
+    auto bwd_data_rows = [&](int t, int64_t r0, int64_t r1) -> int {
+        LocalPart& P = c->parts[t];
+        if (r1 <= r0) return CDFGNN_OK;
+        if (c->cfg.gemm_tf32) {
+            CDF_TRY(gemm_tc_bwd_data(r1 - r0, Fi, Fo, P.S + r0 * ld, ld, c->wpad + c->wpoff[l - 1], ld,
+                                     dZ_prev[t] + r0 * ld_in, ld_in, H_in[t] + r0 * ld_in, ld_in,
+                                     c->cfg.gemm_tf32 == 3, s));
+        } else {
+            launch_gemm_simt(false, true, r1 - r0, Fi, Fo, P.S + r0 * ld, ld, W, Fo, dZ_prev[t] + r0 * ld_in,
+                             ld_in, H_in[t] + r0 * ld_in, ld_in, nullptr, 0, false, s);
+        }
+        c->launches++;
+        return check_launch("gemm bwd_data");
+    };
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
         CDF_TRY(spmm_part(c, P, dZ[t], P.S, ld, s));
         mark(c, PH_GEMM, s);
+        if (c->cfg.gemm_tf32 && t == 0)
+            c->launches += launch_pad_rows(W, Fi, Fo, c->wpad + c->wpoff[l - 1], ld, s);
+        if (ov) CDF_TRY(bwd_data_rows(t, P.B, P.B + P.M));
+    }
+    if (ov) CDF_TRY(launch_gather_async(c, l - 1, 1, dZ_prev, ld_in, eps, s, wire_prev));
+    for (int t = 0; t < c->k; ++t) {
+        LocalPart& P = c->parts[t];
+        mark(c, PH_GEMM, s);
         // dW (+)= H_inᵀ S ; parts accumulate in ascending order
         if (c->cfg.gemm_tf32) {
-            if (t == 0) c->launches += launch_pad_rows(W, Fi, Fo, c->wpad + c->wpoff[l - 1], ld, s);
             const float* Ht = c->trA;
             int64_t ldh = c->npad;
             if (l == 1 && P.xT) {
@@ -701,22 +917,20 @@ int bwd_impl(cdfgnn_ctx* c, int l, float* const* dZ, int64_t ld, const float* co
             c->launches += launch_transpose(P.S, P.n, Fo, ld, c->trB, c->npad, s);
             CDF_TRY(gemm_tc_wgrad(Fi, Fo, P.n, Ht, ldh, c->trB, c->npad, dW, Fo, c->splitk,
                                   c->splitk_cap, t > 0, c->cfg.gemm_tf32 == 3, s, &c->launches));
-            if (dZ_prev) {
-                CDF_TRY(gemm_tc_bwd_data(P.n, Fi, Fo, P.S, ld, c->wpad + c->wpoff[l - 1], ld, dZ_prev[t],
-                                         ld_in, H_in[t], ld_in, c->cfg.gemm_tf32 == 3, s));
-                c->launches++;
-            }
         } else {
             launch_gemm_simt(true, false, Fi, Fo, P.n, H_in[t], ld_in, P.S, ld, dW, Fo, nullptr, 0,
                              c->splitk, c->splitk_cap, t > 0, s);
             c->launches += 2;
-            if (dZ_prev) {
-                launch_gemm_simt(false, true, P.n, Fi, Fo, P.S, ld, W, Fo, dZ_prev[t], ld_in, H_in[t],
-                                 ld_in, nullptr, 0, false, s);
-                c->launches++;
+        }
+        CDF_TRY(check_launch("gemm wgrad"));
+        if (dZ_prev) {
+            if (ov) {
+                CDF_TRY(bwd_data_rows(t, 0, P.B));
+                CDF_TRY(bwd_data_rows(t, P.B + P.M, P.n));
+            } else {
+                CDF_TRY(bwd_data_rows(t, 0, P.n));
             }
         }
-        CDF_TRY(check_launch("gemm bwd"));
     }
     return CDFGNN_OK;
 }
@@ -751,6 +965,7 @@ extern "C" int cdfgnn_cfg_default(cdfgnn_cfg* cfg) {
     cfg->transport = 0;
     cfg->elide_dead_syncs = 1;
     cfg->static_inputs = 0;
+    cfg->overlap = 0;
     return CDFGNN_OK;
 }
 
@@ -810,15 +1025,14 @@ extern "C" int cdfgnn_init(const cdfgnn_plan* plan, const int32_t* parts, int32_
         CUDA_TRY(cudaMemcpyAsync(P.rowptr, P.rowptr_h, sizeof(int32_t) * (P.n + 1), cudaMemcpyHostToDevice, s));
         CUDA_TRY(cudaMemcpyAsync(P.colidx, P.colidx_h, sizeof(int32_t) * P.nnz, cudaMemcpyHostToDevice, s));
         CUDA_TRY(cudaMemcpyAsync(P.val, P.val_h, sizeof(float) * P.nnz, cudaMemcpyHostToDevice, s));
-        {
-            std::vector<int32_t> ord(P.n);
-            for (int64_t r = 0; r < P.n; ++r) ord[r] = (int32_t)r;
-            std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
-                return (P.rowptr_h[x + 1] - P.rowptr_h[x]) > (P.rowptr_h[y + 1] - P.rowptr_h[y]);
-            });
-            CUDA_TRY(cudaMemcpyAsync(P.order, ord.data(), sizeof(int32_t) * P.n, cudaMemcpyHostToDevice, s));
-            CUDA_TRY(cudaStreamSynchronize(s));
+        for (SpmmPlan& S : P.sp) {
+            CUDA_TRY(cudaMemcpyAsync(S.items, S.items_h.data(), sizeof(int2) * S.n_items, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(S.items2, S.items2_h.data(), sizeof(int2) * S.n_items, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(S.split, S.split_h.data(), sizeof(int4) * P.n, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(S.seg_beg, S.seg_beg_h.data(), sizeof(int32_t) * S.seg_beg_h.size(),
+                                     cudaMemcpyHostToDevice, s));
         }
+        CUDA_TRY(cudaStreamSynchronize(s));
         CUDA_TRY(cudaMemcpyAsync(P.halo_local, P.halo_h, sizeof(int32_t) * P.hoff[c->p], cudaMemcpyHostToDevice, s));
         CUDA_TRY(cudaMemcpyAsync(P.moff_d, P.moff.data(), sizeof(int64_t) * (c->p + 1), cudaMemcpyHostToDevice, s));
         CUDA_TRY(cudaMemcpyAsync(P.hoff_d, P.hoff.data(), sizeof(int64_t) * (c->p + 1), cudaMemcpyHostToDevice, s));
@@ -858,6 +1072,13 @@ extern "C" int cdfgnn_init(const cdfgnn_plan* plan, const int32_t* parts, int32_
             }
         }
     }
+    if (cfg->overlap && c->p > 1) {
+        int lo = 0, hi = 0;
+        CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CUDA_TRY(cudaStreamCreateWithPriority(&c->s2, cudaStreamNonBlocking, hi));
+        CUDA_TRY(cudaEventCreateWithFlags(&c->evA, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&c->evB, cudaEventDisableTiming));
+    }
     c->eps = cfg->eps_init;
     c->timing = cfg->timing != 0;
     *out = c.release();
@@ -874,6 +1095,12 @@ extern "C" int cdfgnn_destroy(cdfgnn_ctx* c) {
     if (c->stats_h) cudaFreeHost(c->stats_h);
     if (c->host_scratch) cudaFreeHost(c->host_scratch);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+    if (c->s2) {
+        cudaStreamSynchronize(c->s2);
+        cudaStreamDestroy(c->s2);
+    }
+    if (c->evA) cudaEventDestroy(c->evA);
+    if (c->evB) cudaEventDestroy(c->evB);
     delete c;
     return CDFGNN_OK;
 }
@@ -930,6 +1157,7 @@ static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const
     const int C = c->cfg.dims[L];
     c->launches = 0;
     c->ev_used = 0;
+    std::memset(c->pend, 0, sizeof(c->pend));
     int64_t wire[CDFGNN_MAX_LAYERS][2] = {};
     CUDA_TRY(cudaMemsetAsync(c->stats_d, 0, sizeof(long long) * CDFGNN_MAX_LAYERS * 2 * 4, s));
     CUDA_TRY(cudaMemsetAsync(c->scal_d, 0, sizeof(int32_t) * 8, s));
@@ -987,7 +1215,8 @@ static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const
             dprev[t] = c->parts[t].D[(l - 1) & 1];
         }
         CDF_TRY(bwd_impl(c, l, dcur.data(), ld, h.data(), ldi, W[l - 1], l > 1 ? dprev.data() : nullptr,
-                         c->dW + c->woff[l - 1], eps32, s, &wire[l - 1][1], c->cfg.elide_dead_syncs != 0));
+                         c->dW + c->woff[l - 1], eps32, s, &wire[l - 1][1], c->cfg.elide_dead_syncs != 0,
+                         l > 1 ? &wire[l - 2][1] : nullptr));
         dcur = dprev;
     }
     // ---- parameter aggregation + update (Alg. 1 L12-L13)
@@ -1199,7 +1428,11 @@ extern "C" int cdfgnn_spmm(cdfgnn_ctx* c, int32_t lp, const float* T, float* Y, 
     if (ld % 4 || ld < F || ld > 1024) CDF_FAIL(CDFGNN_EUSAGE, "ld must be a multiple of 4 in [F, 1024]");
     CUDA_TRY(cudaSetDevice(c->device));
     LocalPart& P = c->parts[lp];
-    launch_spmm(P.rowptr, P.colidx, P.val, P.n, T, Y, ld, P.order, (cudaStream_t)stream);
+    const SpmmPlan& S = spmm_plan(P, ld);
+    if (S.nslots && ld > S.pstride)
+        CDF_FAIL(CDFGNN_EUSAGE, "ld %lld exceeds the split-row scratch stride %lld (widest layer)", (long long)ld,
+                 (long long)S.pstride);
+    launch_spmm(P.rowptr, P.colidx, P.val, S.n_items, spmm_items(P, 0, ld), T, Y, ld, (cudaStream_t)stream);
     return check_launch("spmm");
 }
 

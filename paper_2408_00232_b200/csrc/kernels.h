@@ -91,9 +91,22 @@ int launch_scatter_pack_n(const HaloDev& h, const SyncArgs& a, int ntiles, cudaS
 int launch_mirror_apply(const HaloDev& h, const SyncArgs& a, cudaStream_t s);
 
 // ---- SpMM (kernels_spmm.cu): Y[n x ld] = Â T
-// order: row visiting order (degree-descending permutation) or nullptr for identity
-void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val, int64_t n,
-                 const float* T, float* Y, int64_t ld, const int32_t* order, cudaStream_t s);
+// Work items in visiting order: {row, seg} (seg = -1: the whole row; else segment seg of a
+// split row, CSR range [seg_beg[z + seg], seg_beg[z + seg + 1]) with split[row] = {x: first
+// partial slot, y: segments, z: first seg_beg entry}; the row's last finisher sums the
+// partials in segment order).  items == nullptr: identity order, no splitting.
+struct SpmmItems {
+    const int2* items;          // [n_items]
+    const int4* split;          // [n]
+    const int32_t* seg_beg;     // [segments + split rows]
+    float* partial;             // [slots x ld] segment partials
+    int32_t* counter;           // [slots] segments finished per split row (at its first slot; zero at rest)
+};
+int spmm_chunk(bool wide);
+int spmm_default_phases();
+int spmm_phase_min_degree();
+void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val, int64_t n_items,
+                 const SpmmItems& it, const float* T, float* Y, int64_t ld, cudaStream_t s);
 
 // ---- dense (kernels_dense.cu)
 // C[M x ldc] = op(A) op(B) (+ mask) ; columns [N, ldc) of C are written as zero.

@@ -103,7 +103,7 @@ __device__ __forceinline__ int find_seg(const int64_t* off, int p, int64_t idx) 
 // message buffer comes from the decoupled look-back, so the buffer keeps halo-list order.
 // ==================================================================================
 template <int LPR, int VPL, int RPW>
-__global__ void __launch_bounds__(kThreads) gather_pack_kernel(HaloDev h, SyncArgs a) {
+__global__ void __launch_bounds__(kThreads, VPL <= 2 ? 3 : 1) gather_pack_kernel(HaloDev h, SyncArgs a) {
     constexpr int GPW = 32 / LPR;
     constexpr int TR = kWarps * GPW * RPW;
     __shared__ int s_wcnt[kWarps];
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kThreads) gather_pack_kernel(HaloDev h, SyncAr
             const int c0 = (gl + v * LPR) * 4;
             float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f), s4 = make_float4(0.f, 0.f, 0.f, 0.f);
             if (valid && c0 < a.ld) {
-                x4 = ld4(xr + c0);
+                x4 = __ldcs(reinterpret_cast<const float4*>(xr + c0));   // read once: evict-first
                 if (sr) s4 = ld4(sr + c0);
             }
 #pragma unroll
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) gather_pack_kernel(HaloDev h, SyncAr
                     setc(snew, k, sk);
                 }
                 store_codes4(codes, c0, a.F, q);
-                if (sr) st4(sr + c0, snew);     // reading R11: s ← s + deq(q(Δ))
+                if (sr) __stcs(reinterpret_cast<float4*>(sr + c0), snew);   // reading R11: s ← s + deq(q(Δ))
             }
         } else {
             if (gl == 0) reinterpret_cast<uint32_t*>(hdr)[mm] = (uint32_t)ridx[r];
@@ -258,32 +258,69 @@ __global__ void map_kernel(HaloDev h, int mirror_side) {
 // master: one row group per boundary master row
 // ==================================================================================
 template <int LPR, int VPL>
-__global__ void __launch_bounds__(kThreads) master_kernel(HaloDev h, SyncArgs a) {
+__global__ void __launch_bounds__(kThreads, VPL <= 2 ? 4 : 1) master_kernel(HaloDev h, SyncArgs a) {
     constexpr int GPW = 32 / LPR;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane / LPR, gl = lane % LPR;
     const int64_t row = ((int64_t)blockIdx.x * kWarps + warp) * GPW + g;
     const bool valid = row < h.B;
     const int64_t r = valid ? row : 0;
-    float4 acc[VPL];
+    // Independent loads first (aggregate, own value, snapshot, scatter base, and the message
+    // index of every source), so a row costs ~3 dependent memory round trips, not ~3 per source.
+    float* xr = a.X + r * a.ld;
+    float* smr = a.nocache ? nullptr : a.c.s_mas + r * a.ld;
+    float* bmr = a.nocache ? nullptr : a.c.b_mas + r * a.ld;
     const float* aold = a.nocache ? nullptr : a.c.a + r * a.ld;
+    float4 acc[VPL], x[VPL], s4v[VPL], b[VPL];
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
         const int c0 = (gl + v * LPR) * 4;
-        acc[v] = (aold && valid && c0 < a.ld) ? ld4(aold + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const bool in = valid && c0 < a.ld;
+        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        acc[v] = (aold && in) ? ld4(aold + c0) : z4;
+        x[v] = in ? ld4(xr + c0) : z4;
+        s4v[v] = (smr && in) ? ld4(smr + c0) : z4;
+        b[v] = (bmr && in) ? ld4(bmr + c0) : z4;
     }
+    const int nsrc = a.no_msgs ? 0 : h.p;
+    // lane gl of the row group holds source gl's message index (p <= LPR), and its header
+    int32_t mine = -1;
+    float mlo = 0.f, mhi = 0.f;
+    if (nsrc <= LPR) {
+        if (valid && gl < nsrc && gl != h.me) {
+            mine = h.idxmap[(int64_t)gl * h.B + r];
+            if (mine >= 0 && h.quant) {
+                const uint32_t* hp = reinterpret_cast<const uint32_t*>(h.grecv->hdr[gl] + (int64_t)mine * 12);
+                mlo = __uint_as_float(hp[1]);
+                mhi = __uint_as_float(hp[2]);
+            }
+        }
+    }
+    const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (g * LPR));
+    const unsigned have = (__ballot_sync(0xffffffffu, mine >= 0) & gmask) >> (g * LPR);
     bool any_msg = false;
     // Alg. 2 L11-L13: received Δ in ascending source part (R13)
-    for (int s = 0; s < (a.no_msgs ? 0 : h.p); ++s) {
+    for (int s = 0; s < nsrc; ++s) {
         if (s == h.me) continue;
-        const int32_t m = valid ? h.idxmap[(int64_t)s * h.B + r] : -1;
-        if (m < 0) continue;
+        int32_t m;
+        float lo = 0.f, hi = 0.f;
+        if (nsrc <= LPR) {
+            if (!((have >> s) & 1u)) continue;
+            m = __shfl_sync(gmask, mine, g * LPR + s);
+            lo = __shfl_sync(gmask, mlo, g * LPR + s);
+            hi = __shfl_sync(gmask, mhi, g * LPR + s);
+        } else {
+            m = valid ? h.idxmap[(int64_t)s * h.B + r] : -1;
+            if (m < 0) continue;
+            if (h.quant) {
+                const uint32_t* hp = reinterpret_cast<const uint32_t*>(h.grecv->hdr[s] + (int64_t)m * 12);
+                lo = __uint_as_float(hp[1]);
+                hi = __uint_as_float(hp[2]);
+            }
+        }
         any_msg = true;
-        const uint8_t* hdr = h.grecv->hdr[s];
         const uint8_t* pay = h.grecv->pay[s];
         if (h.quant) {
-            const uint32_t* hp = reinterpret_cast<const uint32_t*>(hdr + (int64_t)m * 12);
-            const float lo = __uint_as_float(hp[1]), hi = __uint_as_float(hp[2]);
             const float stp = step8(lo, hi);
             const uint8_t* codes = pay + (int64_t)m * a.F;
 #pragma unroll
@@ -310,26 +347,18 @@ __global__ void __launch_bounds__(kThreads) master_kernel(HaloDev h, SyncArgs a)
         }
     }
     // Alg. 2 L14-L19: the master's own replica, unquantised
-    float* xr = a.X + r * a.ld;
-    float* smr = a.nocache ? nullptr : a.c.s_mas + r * a.ld;
-    float4 x[VPL], dd[VPL];
+    float4 dd[VPL];
     float maxd = 0.f, maxs = 0.f;
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
         const int c0 = (gl + v * LPR) * 4;
-        x[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid && c0 < a.ld) {
-            x[v] = ld4(xr + c0);
-            if (smr) s4 = ld4(smr + c0);
-        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const float dk = __fsub_rn(comp(x[v], k), comp(s4, k));
+            const float dk = __fsub_rn(comp(x[v], k), comp(s4v[v], k));
             setc(dd[v], k, dk);
             if (c0 + k < a.F) {
                 maxd = fmaxf(maxd, fabsf(dk));
-                maxs = fmaxf(maxs, fabsf(comp(s4, k)));
+                maxs = fmaxf(maxs, fabsf(comp(s4v[v], k)));
             }
         }
     }
@@ -357,13 +386,6 @@ __global__ void __launch_bounds__(kThreads) master_kernel(HaloDev h, SyncArgs a)
         }
     }
     // Alg. 2 L20-L22 / R12: scatter delta staged once; every replica applies the same codes
-    float* bmr = a.nocache ? nullptr : a.c.b_mas + r * a.ld;
-    float4 b[VPL];
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-        const int c0 = (gl + v * LPR) * 4;
-        b[v] = (bmr && valid && c0 < a.ld) ? ld4(bmr + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
     // scatter delta and its range, reduced by every lane of the warp (shuffles stay converged)
     float4 del[VPL];
     float lo = INFINITY, hi = -INFINITY;

@@ -1,23 +1,20 @@
 // Local CSR SpMM  Y = Â_i T  (eq. 1; Alg. 1 L3).
 //
-// Row-group-per-row CSR: LPR lanes own one output row, each lane VPL float4
-// column chunks, so every neighbour's feature row is one coalesced 16-byte-per-
-// lane read (ld % 4 == 0, reading R24).  The group first loads LPR (col, val)
-// pairs cooperatively (one coalesced load each) and broadcasts them with
-// shuffles; UNR neighbours are in flight per lane before the FMAs.  The sum
-// over a row's neighbours runs in CSR order, so results are run-to-run
-// deterministic.
+// Row-group-per-item CSR: LPR lanes own one work item, each lane VPL float4 column
+// chunks, so every neighbour's feature row is one coalesced 16-byte-per-lane read
+// (ld % 4 == 0, reading R24).  The group first loads LPR (col, val) pairs
+// cooperatively (one coalesced load each) and broadcasts them with shuffles; UNR
+// neighbours are in flight per lane before the FMAs.
 //
-// Rows are visited in longest-first order (a degree-descending permutation built
-// at init): power-law hubs start first and the short rows fill the tail, and the
-// warps of a block get rows of similar length (ncu r1: long-scoreboard stalls with
-// only 19 of 32 resident warps active under the identity order).
-//
-// Wide rows (ld > panel) can be processed in column panels, panel-major across the
-// grid: while one panel is in flight its slice of T (n x panel x 4 B) stays
-// resident in the 126 MB L2 instead of being streamed from HBM once per
-// neighbour (profiles/r1: 52.7 GB of DRAM reads per unpanelled
-// 256-wide launch on C3 vs 1.4 GB compulsory).
+// Work items (built once at init, SpmmItems): a row, or one segment of a split row.
+// Segments are either fixed-length chunks (a power-law hub row is a chain of dependent
+// L2 round trips whose latency can set a short launch's critical path) or column
+// phases (all split rows' neighbours in column range k are visited before range k+1,
+// so the slice of T being gathered is an L2-sized window).  Each segment writes its
+// partial row to a scratch slot, and the group that completes a row's last segment
+// (atomic counter) sums the partials in segment order, so results are bitwise
+// run-to-run deterministic regardless of which warp finishes last.  Unsplit rows are
+// visited longest-first (LPT).
 #include <algorithm>
 #include <cstdlib>
 
@@ -29,36 +26,43 @@ namespace {
 constexpr int kThreads = 256;
 
 template <int LPR, int VPL, int UNR, int TAIL>
-__global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n, const int32_t* __restrict__ rowptr,
+__global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n_items, const int32_t* __restrict__ rowptr,
                                                         const int32_t* __restrict__ colidx,
                                                         const float* __restrict__ val,
                                                         const float* __restrict__ T,
-                                                        float* __restrict__ Y, int64_t ld, int pw,
-                                                        int64_t blocks_per_panel,
-                                                        const int32_t* __restrict__ order) {
+                                                        float* __restrict__ Y, int64_t ld,
+                                                        SpmmItems it, int stream) {
     constexpr int GPW = 32 / LPR;
     const int lane = threadIdx.x & 31;
     const int g = lane / LPR, gl = lane % LPR;
     const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (g * LPR));
-    const int64_t panel = blockIdx.x / blocks_per_panel;
-    const int64_t blk = blockIdx.x - panel * blocks_per_panel;
-    const int64_t slot = (blk * (kThreads / 32) + (threadIdx.x >> 5)) * GPW + g;
-    if (slot >= n) return;
-    const int64_t row = order ? __ldg(order + slot) : slot;
-    const int col0 = (int)panel * pw;
-    const int width = min((int64_t)pw, ld - col0);
-    const float* Tp = T + col0;
-    const int beg = __ldg(rowptr + row), end = __ldg(rowptr + row + 1);
+    const int64_t slot = ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * GPW + g;
+    if (slot >= n_items) return;
+    int64_t row = slot;
+    int chunk = -1;
+    if (it.items) {
+        const int2 w = __ldg(it.items + slot);
+        row = w.x;
+        chunk = w.y;
+    }
+    const int rb = __ldg(rowptr + row), re = __ldg(rowptr + row + 1);
+    int beg = rb, end = re;
+    int4 sp = make_int4(0, 0, 0, 0);
+    if (chunk >= 0) {
+        sp = __ldg(it.split + row);
+        beg = __ldg(it.seg_beg + sp.z + chunk);
+        end = __ldg(it.seg_beg + sp.z + chunk + 1);
+    }
     float4 acc[VPL];
 #pragma unroll
     for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     bool colok[VPL];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) colok[v] = (gl + v * LPR) * 4 < width;
+    for (int v = 0; v < VPL; ++v) colok[v] = (gl + v * LPR) * 4 < ld;
     for (int base = beg; base < end; base += LPR) {
         const int e = base + gl;
-        const int c = e < end ? __ldg(colidx + e) : 0;
-        const float w = e < end ? __ldg(val + e) : 0.f;
+        const int c = e < end ? (stream ? __ldcs(colidx + e) : __ldg(colidx + e)) : 0;
+        const float w = e < end ? (stream ? __ldcs(val + e) : __ldg(val + e)) : 0.f;
         const int cnt = min(LPR, end - base);
         if (TAIL == 0) {
             // full batches of UNR neighbours, then the remainder one at a time
@@ -74,7 +78,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n, const int32_t
                 float4 t[UNR][VPL];
 #pragma unroll
                 for (int u = 0; u < UNR; ++u) {
-                    const float* tr = Tp + (int64_t)ck[u] * ld;
+                    const float* tr = T + (int64_t)ck[u] * ld;
 #pragma unroll
                     for (int v = 0; v < VPL; ++v)
                         t[u][v] = colok[v] ? __ldg(reinterpret_cast<const float4*>(tr + (gl + v * LPR) * 4))
@@ -93,7 +97,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n, const int32_t
             for (; k < cnt; ++k) {
                 const int ck = __shfl_sync(gmask, c, k, LPR);
                 const float wk = __shfl_sync(gmask, w, k, LPR);
-                const float* tr = Tp + (int64_t)ck * ld;
+                const float* tr = T + (int64_t)ck * ld;
 #pragma unroll
                 for (int v = 0; v < VPL; ++v) {
                     if (!colok[v]) continue;
@@ -119,7 +123,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n, const int32_t
                 float4 t[UNR][VPL];
 #pragma unroll
                 for (int u = 0; u < UNR; ++u) {
-                    const float* tr = Tp + (int64_t)ck[u] * ld;
+                    const float* tr = T + (int64_t)ck[u] * ld;
                     const bool live = k + u < cnt;
 #pragma unroll
                     for (int v = 0; v < VPL; ++v)
@@ -138,24 +142,61 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n, const int32_t
             }
         }
     }
-    float* yr = Y + row * ld + col0;
+    if (chunk >= 0) {
+        // split row: publish this chunk's partial; the last of the row's chunks to finish
+        // sums all partials in chunk order (fixed order => deterministic bits)
+        const int pbase = sp.x, nch = sp.y;
+        float* pr = it.partial + (int64_t)(pbase + chunk) * ld;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+            if (colok[v]) __stcg(reinterpret_cast<float4*>(pr + (gl + v * LPR) * 4), acc[v]);
+        __threadfence();
+        int last = 0;
+        if (gl == 0) last = atomicAdd(it.counter + pbase, 1) == nch - 1;
+        last = __shfl_sync(gmask, last, 0, LPR);
+        if (!last) return;
+        __threadfence();
+        float4 sum[VPL];
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) sum[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int cc = 0; cc < nch; ++cc) {
+            const float* qr = it.partial + (int64_t)(pbase + cc) * ld;
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                if (!colok[v]) continue;
+                const float4 q = cc == chunk ? acc[v] : __ldcg(reinterpret_cast<const float4*>(qr + (gl + v * LPR) * 4));
+                if (cc == 0) {
+                    sum[v] = q;
+                } else {
+                    sum[v].x = __fadd_rn(sum[v].x, q.x);
+                    sum[v].y = __fadd_rn(sum[v].y, q.y);
+                    sum[v].z = __fadd_rn(sum[v].z, q.z);
+                    sum[v].w = __fadd_rn(sum[v].w, q.w);
+                }
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) acc[v] = sum[v];
+        if (gl == 0) it.counter[pbase] = 0;     // re-armed for the next launch
+    }
+    float* yr = Y + row * ld;
 #pragma unroll
     for (int v = 0; v < VPL; ++v)
-        if (colok[v]) *reinterpret_cast<float4*>(yr + (gl + v * LPR) * 4) = acc[v];
+        if (colok[v]) {
+            float4* yp = reinterpret_cast<float4*>(yr + (gl + v * LPR) * 4);
+            if (stream) __stcs(yp, acc[v]); else *yp = acc[v];
+        }
 }
 
 template <int LPR, int VPL, int UNR>
 void launch(int64_t n, const int32_t* rowptr, const int32_t* colidx, const float* val, const float* T, float* Y,
-            int64_t ld, int pw, const int32_t* order, cudaStream_t s, int tail) {
+            int64_t ld, const SpmmItems& it, cudaStream_t s, int tail, int stream) {
     const int64_t rows_per_block = (kThreads / 32) * (32 / LPR);
-    const int64_t bpp = (n + rows_per_block - 1) / rows_per_block;
-    const int64_t panels = (ld + pw - 1) / pw;
+    const unsigned grid = (unsigned)((n + rows_per_block - 1) / rows_per_block);
     if (tail)
-        spmm_kernel<LPR, VPL, UNR, 1><<<(unsigned)(bpp * panels), kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y,
-                                                                                    ld, pw, bpp, order);
+        spmm_kernel<LPR, VPL, UNR, 1><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, it, stream);
     else
-        spmm_kernel<LPR, VPL, UNR, 0><<<(unsigned)(bpp * panels), kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y,
-                                                                                    ld, pw, bpp, order);
+        spmm_kernel<LPR, VPL, UNR, 0><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, it, stream);
 }
 
 int env_int(const char* name, int dflt) {
@@ -165,31 +206,36 @@ int env_int(const char* name, int dflt) {
 
 }  // namespace
 
-void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val, int64_t n,
-                 const float* T, float* Y, int64_t ld, const int32_t* order, cudaStream_t s) {
-    if (n <= 0) return;
-    if (env_int("CDFGNN_SPMM_IDENTITY", 0)) order = nullptr;
-    int pw = env_int("CDFGNN_SPMM_PANEL", 256);
-    if (pw < 4 || pw % 4) pw = 256;
-    pw = (int)std::min<int64_t>(pw, ld);
-    const int nv = pw / 4;      // float4 per row within a panel
+// chunk length for the wide (ld > 64) and narrow row classes; 0 = no chunking
+int spmm_chunk(bool wide) {
+    return wide ? env_int("CDFGNN_SPMM_CHUNK_WIDE", 0) : env_int("CDFGNN_SPMM_CHUNK", 2048);
+}
+int spmm_default_phases() { return env_int("CDFGNN_SPMM_PHASES", 1); }
+int spmm_phase_min_degree() { return env_int("CDFGNN_SPMM_PHASE_MIN", 64); }
+
+void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val, int64_t n_items,
+                 const SpmmItems& it, const float* T, float* Y, int64_t ld, cudaStream_t s) {
+    if (n_items <= 0) return;
+    const int nv = (int)(ld / 4);      // float4 per row
     const int unr = env_int("CDFGNN_SPMM_UNR", 0);
     const int tail = env_int("CDFGNN_SPMM_TAIL", ld > 64 ? 1 : 0);   // predicated tail for wide rows
-    if (nv <= 2) launch<2, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
-    else if (nv <= 4) launch<4, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
-    else if (nv <= 8) launch<8, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
+    // narrow rows: stream the CSR arrays and the output past L2 (evict-first), keeping T's lines
+    const int stream = env_int("CDFGNN_SPMM_STREAM", ld <= 64 ? 1 : 0);
+    if (nv <= 2) launch<2, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+    else if (nv <= 4) launch<4, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+    else if (nv <= 8) launch<8, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
     else if (nv <= 16) {
-        if (unr == 4) launch<16, 1, 4>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
-        else launch<16, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
+        if (unr == 4) launch<16, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+        else launch<16, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
     } else if (nv <= 32) {
-        if (unr == 4) launch<32, 1, 4>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
-        else launch<32, 1, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
+        if (unr == 4) launch<32, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+        else launch<32, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
     } else if (nv <= 64) {
-        if (unr == 2) launch<32, 2, 2>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
-        else if (unr == 8) launch<32, 2, 8>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
-        else launch<32, 2, 4>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
-    } else if (nv <= 128) launch<32, 4, 4>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
-    else launch<32, 8, 2>(n, rowptr, colidx, val, T, Y, ld, pw, order, s, tail);
+        if (unr == 2) launch<32, 2, 2>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+        else if (unr == 8) launch<32, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+        else launch<32, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+    } else if (nv <= 128) launch<32, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+    else launch<32, 8, 2>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
 }
 
 }  // namespace cdfgnn

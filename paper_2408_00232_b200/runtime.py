@@ -33,7 +33,7 @@ class Run:
                  timing: bool = False, plan: Optional[api.Plan] = None,
                  host_inputs: bool = False, partition_kw: Optional[Dict] = None,
                  gemm: str = "tf32x3", transport: str = "push", elide: bool = True,
-                 static_inputs: bool = False):
+                 static_inputs: bool = False, overlap: bool = False):
         import torch
         self.torch = torch
         self.ds = ds
@@ -47,7 +47,8 @@ class Run:
                                    optimizer=1 if optimizer == "adam" else 0, lr=lr,
                                    timing=int(timing), gemm_tf32=GEMM_MODES[gemm],
                                    transport={"push": 0, "nccl": 1}[transport],
-                                   elide_dead_syncs=int(elide), static_inputs=int(static_inputs))
+                                   elide_dead_syncs=int(elide), static_inputs=int(static_inputs),
+                                   overlap=int(overlap))
         nbytes = api.workspace_size(self.plan, self.parts, self.cfg)
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         uid = None

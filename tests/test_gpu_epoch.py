@@ -138,18 +138,26 @@ def test_label_out_of_range_is_edata():
     run.close()
 
 
-@pytest.mark.parametrize("cache,quant", [(True, 8), (False, 0)])
-def test_dead_sync_elision_and_static_inputs_are_bitwise_neutral(cache, quant):
-    """§8 f2: skipping the layer-L forward scatter and backward gather, and reusing Xᵀ,
-    change no bit of the trajectory."""
+@pytest.mark.parametrize("cache,quant,dims", [(True, 8, (20, 24, 6)), (False, 0, (20, 24, 6)),
+                                              (True, 8, (20, 24, 16, 6)), (True, 0, (20, 24, 16, 6))])
+def test_dead_sync_elision_static_inputs_and_overlap_are_bitwise_neutral(cache, quant, dims):
+    """§8 f2: skipping the layer-L forward scatter and backward gather, and reusing Xᵀ;
+    §8 f1: boundary-rows-first scheduling with the gather on a second stream — none of them
+    changes a bit of the trajectory."""
     torch = require_gpu()
-    d = small_random_graph(1200, 8000, (20, 24, 6), seed=65)
-    runs = [Run(d, 3, cache=cache, quant_bits=quant, eps0=0.01, elide=e, static_inputs=si)
-            for e, si in ((False, False), (True, True))]
+    d = small_random_graph(1200, 8000, dims, seed=65)
+    runs = [Run(d, 3, cache=cache, quant_bits=quant, eps0=0.01, elide=e, static_inputs=si, overlap=ov)
+            for e, si, ov in ((False, False, False), (True, True, False), (True, True, True))]
     for ep in range(4):
         res = [r.epoch() for r in runs]
-        assert res[0]["loss"] == res[1]["loss"]
-        for wa, wb in zip(runs[0].weights(), runs[1].weights()):
-            assert np.array_equal(wa, wb)
+        for r in res[1:]:
+            assert r["loss"] == res[0]["loss"]
+        # same schedule of syncs (elision on): the overlapped run sends exactly the same messages
+        for a, b in zip(res[2]["fwd"] + res[2]["bwd"], res[1]["fwd"] + res[1]["bwd"]):
+            assert (a["gather_sent"], a["master_fired"], a["scatter_msgs"]) == \
+                (b["gather_sent"], b["master_fired"], b["scatter_msgs"])
+        for r in runs[1:]:
+            for wa, wb in zip(runs[0].weights(), r.weights()):
+                assert np.array_equal(wa, wb)
     for r in runs:
         r.close()

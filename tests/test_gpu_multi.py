@@ -14,9 +14,10 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("mode", ["exact", "cache_int8"])
-@pytest.mark.parametrize("transport", ["push", "nccl"])
-def test_two_gpus_match_one_gpu(mode, transport):
+@pytest.mark.parametrize("mode,transport,overlap", [("exact", "push", 0), ("cache_int8", "push", 0),
+                                                    ("exact", "nccl", 0), ("cache_int8", "nccl", 0),
+                                                    ("cache_int8", "push", 1)])
+def test_two_gpus_match_one_gpu(mode, transport, overlap):
     torch = require_gpu()
     n = torch.cuda.device_count()
     if n < 2:
@@ -24,7 +25,7 @@ def test_two_gpus_match_one_gpu(mode, transport):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
            "--master-addr", "127.0.0.1", "--master-port", "29517",
            os.path.join(ROOT, "tools", "mgpu_check.py"), "--mode", mode, "--epochs", "4",
-           "--transport", transport]
+           "--transport", transport, "--overlap", str(overlap)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

@@ -13,6 +13,7 @@ def main():
     ap.add_argument("--p", type=int, default=4)
     ap.add_argument("--epochs", type=int, default=3)
     ap.add_argument("--mode", default="cache_int8")
+    ap.add_argument("--overlap", type=int, default=0)
     a = ap.parse_args()
     import torch
     from paper_2408_00232_b200.runtime import Run
@@ -21,7 +22,8 @@ def main():
     ds = cached_dataset(get_config(a.config))
     cache, quant = {"cache_int8": (True, 8), "cache_fp32": (True, 0), "quant_only": (False, 8),
                     "nocache": (False, 0)}[a.mode]
-    run = Run(ds, a.p, cache=cache, quant_bits=quant, timing=True)
+    run = Run(ds, a.p, cache=cache, quant_bits=quant, timing=True, overlap=bool(a.overlap),
+              static_inputs=True)
     for e in range(a.epochs):
         st = run.epoch()
         print(json.dumps({"epoch": e, "loss": st["loss"], "gemm": round(st["ms_gemm"], 3),

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--epochs", type=int, default=5)
     ap.add_argument("--mode", default="cache_int8")
     ap.add_argument("--transport", default="push")
+    ap.add_argument("--overlap", type=int, default=0)
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -41,7 +42,8 @@ def main():
     eps0 = 0.0 if a.mode == "exact" else 0.01
     kw = dict(cache=cache, quant_bits=quant, eps0=eps0, adaptive=a.mode != "exact",
               optimizer="adam", lr=0.01)
-    run = Run(ds, world, rank=rank, world=world, device=local, transport=a.transport, **kw)
+    run = Run(ds, world, rank=rank, world=world, device=local, transport=a.transport,
+              overlap=bool(a.overlap), **kw)
     ref = Run(ds, world, device=local, plan=run.plan, **kw) if rank == 0 else None
     ok = True
     rows = []
