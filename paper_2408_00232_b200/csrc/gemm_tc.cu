@@ -72,6 +72,23 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// TMA bulk store of a 32 x 32 fp32 box from 128-B-swizzled shared memory
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -128,11 +145,15 @@ struct Cfg {
     static constexpr int TMA_BYTES = A_BYTES + B_BYTES;                  // fp32 (or tf32) tiles
     static constexpr int STAGE_BYTES = TMA_BYTES * (SPLIT3 ? 2 : 1);     // + lo parts for 3xTF32
     static constexpr int STAGES = (SPLIT3 ? 196608 : 200704) / STAGE_BYTES;
-    static constexpr int EPI_BYTES = kEpiWarps * 32 * 33 * 4;            // epilogue transpose staging
+    static constexpr int EPI_BYTES = kEpiWarps * 32 * 32 * 4;            // epilogue staging (TMA store boxes)
     static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;        // double-buffered accumulator
 };
 
+#ifndef GEMM_HI_INPLACE
+#define GEMM_HI_INPLACE 0
+#endif
+__device__ __forceinline__ float tf32_tr(float x) { return __uint_as_float(__float_as_uint(x) & ~0x1FFFu); }
 __device__ __forceinline__ float tf32_rn(float x) {
     uint32_t u = __float_as_uint(x);
     u = (u + 0xFFFu + ((u >> 13) & 1u)) & ~0x1FFFu;      // round to nearest even, 10-bit mantissa
@@ -147,6 +168,7 @@ struct EpiArgs {
     float* ws;         // split-K partials [z][M][ldw]
     int64_t ldw;
     int accumulate;
+    int tma;           // 1: stores through the C tensor map (2-D {ldc, M}; 3-D {ldw, M, splits} for ws)
 };
 
 // Persistent, warp-specialised tcgen05 GEMM.  One CTA per SM walks the output tiles
@@ -158,8 +180,9 @@ struct EpiArgs {
 //   warps 6-9       epilogue: tcgen05.ld 32 lanes each -> mask / zero padding / split-K partial
 template <bool A_MN, bool B_MN, int BN, bool SPLIT3>
 __global__ void __launch_bounds__(kThreads, 1)
-gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                 int total_kb, int kb_per_split, int m_tiles, int n_tiles, int z_tiles, EpiArgs ep) {
+gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmC, int M, int N, int total_kb, int kb_per_split, int m_tiles,
+                 int n_tiles, int z_tiles, EpiArgs ep) {
     using C_ = Cfg<BN, SPLIT3>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -315,12 +338,22 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     float4* lo = reinterpret_cast<float4*>(stA(s) + C_::TMA_BYTES);
 #pragma unroll 4
                     for (int v = ct; v < NV; v += 32 * kConvWarps) {
+#if GEMM_HI_INPLACE
                         const float4 x = base[v];
                         float4 h, l;
                         h.x = tf32_rn(x.x); h.y = tf32_rn(x.y); h.z = tf32_rn(x.z); h.w = tf32_rn(x.w);
                         l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
                         base[v] = h;
                         lo[v] = l;
+#else
+                        // hi = the raw fp32 word: kind::tf32 reads only its top 19 bits (truncation,
+                        // tools/tc_raw.cu), so lo = x − trunc(x) is exact and only lo is written
+                        const float4 x = base[v];
+                        float4 l;
+                        l.x = x.x - tf32_tr(x.x); l.y = x.y - tf32_tr(x.y);
+                        l.z = x.z - tf32_tr(x.z); l.w = x.w - tf32_tr(x.w);
+                        lo[v] = l;
+#endif
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to tcgen05
                     __syncwarp();
@@ -341,71 +374,61 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             const uint32_t aph = (uint32_t)(ti >> 1) & 1u;
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
-            // each lane holds one accumulator row; 32x32 chunks are transposed through shared
-            // memory so every global store instruction writes 4 full 128-byte row segments
-            float* st = epi_smem + (warp - kEpiWarp0) * 32 * 33;
+            // each lane holds one accumulator row (32 consecutive columns per tcgen05.ld)
+            float* st = epi_smem + (warp - kEpiWarp0) * 32 * 32;     // 4 KB, 1024-B aligned
             const int rbase = m0 + 32 * q;
-            const bool vec = (ep.ws ? (ep.ldw & 3) == 0 : (ep.ldc & 3) == 0) &&
-                             (!ep.mask || (ep.ldm & 3) == 0);
+            const int row = rbase + lane;
+            const int64_t ldo = ep.ws ? ep.ldw : ep.ldc;
+            const int z = t / (m_tiles * n_tiles);
 #pragma unroll 1
             for (int c0 = 32 * eg; c0 < BN; c0 += 64) {
+                const int col0 = n0 + c0;
+                if (col0 >= ldo) break;                        // warp-uniform
+                // masks for this lane's row segment, in flight with the TMEM load
+                float4 mk[8];
+                if (ep.mask) {
+                    const float* mrow = ep.mask + (int64_t)row * ep.ldm + col0;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        mk[j] = (row < M && col0 + 4 * j < ldo) ? *reinterpret_cast<const float4*>(mrow + 4 * j)
+                                                               : make_float4(1.f, 1.f, 1.f, 1.f);
+                }
                 float v[32];
                 tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c0), v);
-                const int col0 = n0 + c0;
-                const int64_t ldo = ep.ws ? ep.ldw : ep.ldc;
-                if (col0 >= ldo) continue;                     // warp-uniform
-                float* obase = ep.ws ? ep.ws + (int64_t)(t / (m_tiles * n_tiles)) * M * ep.ldw : ep.C;
-                if (vec) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) st[lane * 33 + j] = v[j];
-                    __syncwarp();
-                    const int rr = lane >> 3, cc = (lane & 7) * 4;
-                    const int col = col0 + cc;
-                    // masks (and accumulate inputs) for all 8 row groups in flight together
-                    float4 mk[8], ci[8];
-#pragma unroll
-                    for (int g = 0; g < 8; ++g) {
-                        const int row = rbase + 4 * g + rr;
-                        const bool ok = row < M && col < ldo;
-                        mk[g] = (ep.mask && ok) ? *reinterpret_cast<const float4*>(ep.mask + (int64_t)row * ep.ldm + col)
-                                                : make_float4(1.f, 1.f, 1.f, 1.f);
-                        ci[g] = (ep.accumulate && !ep.ws && ok)
-                                    ? *reinterpret_cast<const float4*>(obase + (int64_t)row * ldo + col)
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int j = 0; j < 32; ++j) {
+                    if (col0 + j >= N) v[j] = 0.f;             // zero padding columns
+                    if (ep.mask) {
+                        const float mj = (j & 3) == 0 ? mk[j >> 2].x : (j & 3) == 1 ? mk[j >> 2].y
+                                       : (j & 3) == 2 ? mk[j >> 2].z : mk[j >> 2].w;
+                        if (!(mj > 0.f)) v[j] = 0.f;
                     }
-#pragma unroll
-                    for (int g = 0; g < 8; ++g) {
-                        const int i = 4 * g;
-                        const int row = rbase + i + rr;
-                        if (row < M && col < ldo) {
-                            float4 o;
-                            o.x = col + 0 < N ? st[(i + rr) * 33 + cc + 0] : 0.f;
-                            o.y = col + 1 < N ? st[(i + rr) * 33 + cc + 1] : 0.f;
-                            o.z = col + 2 < N ? st[(i + rr) * 33 + cc + 2] : 0.f;
-                            o.w = col + 3 < N ? st[(i + rr) * 33 + cc + 3] : 0.f;
-                            if (!(mk[g].x > 0.f)) o.x = 0.f;
-                            if (!(mk[g].y > 0.f)) o.y = 0.f;
-                            if (!(mk[g].z > 0.f)) o.z = 0.f;
-                            if (!(mk[g].w > 0.f)) o.w = 0.f;
-                            o.x += ci[g].x; o.y += ci[g].y; o.z += ci[g].z; o.w += ci[g].w;
-                            *reinterpret_cast<float4*>(obase + (int64_t)row * ldo + col) = o;
-                        }
-                    }
+                }
+                if (ep.tma) {
+                    // 128-B swizzled 32 x 32 box: lane r's 16-byte chunk j lives at chunk j ^ (r & 7)
+                    if (lane == 0) bulk_wait_read0();           // the previous box has left st
                     __syncwarp();
-                } else {
-                    const int row = rbase + lane;
-                    if (row < M) {
-                        float* orow = obase + (int64_t)row * ldo;
-                        const float* mrow = ep.mask ? ep.mask + (int64_t)row * ep.ldm : nullptr;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const int col = col0 + j;
-                            if (col >= ldo) break;
-                            float o = col < N ? v[j] : 0.f;
-                            if (mrow && col < N && !(mrow[col] > 0.f)) o = 0.f;
-                            if (ep.accumulate && !ep.ws && col < N) o += orow[col];
-                            orow[col] = o;
-                        }
+                    for (int j = 0; j < 8; ++j)
+                        *reinterpret_cast<float4*>(st + lane * 32 + ((j ^ (lane & 7)) * 4)) =
+                            make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (ep.ws) tma_store_3d(&tmC, st, col0, rbase, z);
+                        else tma_store_2d(&tmC, st, col0, rbase);
+                        bulk_commit();
+                    }
+                } else if (row < M) {
+                    float* obase = ep.ws ? ep.ws + (int64_t)z * M * ep.ldw : ep.C;
+                    float* orow = obase + (int64_t)row * ldo;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int col = col0 + j;
+                        if (col >= ldo) break;
+                        float o = v[j];
+                        if (ep.accumulate && !ep.ws && col < N) o += orow[col];
+                        orow[col] = o;
                     }
                 }
             }
@@ -415,6 +438,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc])) : "memory");
         }
     }
+    if (warp >= kEpiWarp0 && lane == 0) bulk_wait0();      // TMA stores complete before exit
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -513,9 +537,26 @@ bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int
     return r == CUDA_SUCCESS;
 }
 
+// Output map for the TMA-store epilogue: fp32 [z][rows][cols] (row stride ld), box {32, 32, 1},
+// 128-B swizzle; out-of-range rows / columns of a box are clipped by the TMA unit.
+bool make_store_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld, int64_t zs,
+                    bool three_d) {
+    EncodeFn fn = encode_fn();
+    if (!fn || (reinterpret_cast<uintptr_t>(base) & 15) || (ld & 3)) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)zs};
+    cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), (cuuint64_t)(ld * 4 * rows)};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    const cuuint32_t rank = three_d ? 3 : 2;
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 template <bool A_MN, bool B_MN, int BN, bool SPLIT3>
-int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, int64_t M, int64_t N, int64_t K, int splits,
-                   const EpiArgs& ep, cudaStream_t s) {
+int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, int64_t M, int64_t N,
+                   int64_t K, int splits, const EpiArgs& ep, cudaStream_t s) {
     using C_ = Cfg<BN, SPLIT3>;
     static bool attr = false;
     auto kern = gemm_tf32_kernel<A_MN, B_MN, BN, SPLIT3>;
@@ -537,23 +578,33 @@ int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, int64_t M, int6
         if (sms <= 0) sms = 148;
     }
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
-    kern<<<grid, kThreads, C_::SMEM, s>>>(ta, tb, (int)M, (int)N, total_kb, kbps, mt, nt, zs, ep);
+    kern<<<grid, kThreads, C_::SMEM, s>>>(ta, tb, tc, (int)M, (int)N, total_kb, kbps, mt, nt, zs, ep);
     return cudaGetLastError() == cudaSuccess ? CDFGNN_OK : CDFGNN_ECUDA;
 }
 
 template <bool A_MN, bool B_MN>
-int launch_bn(int BN, bool split3, const CUtensorMap& ta, const CUtensorMap& tb, int64_t M, int64_t N, int64_t K,
-              int splits, const EpiArgs& ep, cudaStream_t s) {
+int launch_bn(int BN, bool split3, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, int64_t M,
+              int64_t N, int64_t K, int splits, const EpiArgs& ep, cudaStream_t s) {
     if (split3) {
-        if (BN == 64) return launch_variant<A_MN, B_MN, 64, true>(ta, tb, M, N, K, splits, ep, s);
-        return launch_variant<A_MN, B_MN, 128, true>(ta, tb, M, N, K, splits, ep, s);
+        if (BN == 64) return launch_variant<A_MN, B_MN, 64, true>(ta, tb, tc, M, N, K, splits, ep, s);
+        if (BN == 128) return launch_variant<A_MN, B_MN, 128, true>(ta, tb, tc, M, N, K, splits, ep, s);
+        return launch_variant<A_MN, B_MN, 256, true>(ta, tb, tc, M, N, K, splits, ep, s);
     }
-    if (BN == 64) return launch_variant<A_MN, B_MN, 64, false>(ta, tb, M, N, K, splits, ep, s);
-    if (BN == 128) return launch_variant<A_MN, B_MN, 128, false>(ta, tb, M, N, K, splits, ep, s);
-    return launch_variant<A_MN, B_MN, 256, false>(ta, tb, M, N, K, splits, ep, s);
+    if (BN == 64) return launch_variant<A_MN, B_MN, 64, false>(ta, tb, tc, M, N, K, splits, ep, s);
+    if (BN == 128) return launch_variant<A_MN, B_MN, 128, false>(ta, tb, tc, M, N, K, splits, ep, s);
+    return launch_variant<A_MN, B_MN, 256, false>(ta, tb, tc, M, N, K, splits, ep, s);
 }
 
-int pick_bn(int64_t N, bool split3) { return N <= 64 ? 64 : ((N <= 128 || split3) ? 128 : 256); }
+// 3xTF32 at N = 256 keeps two 96 KB stages; the wider MMA halves the shared-memory
+// operand traffic per flop (GEMM_SPLIT3_BN256=0 restores the 128-wide tile)
+#ifndef GEMM_SPLIT3_BN256
+#define GEMM_SPLIT3_BN256 1
+#endif
+int pick_bn(int64_t N, bool split3) {
+    if (N <= 64) return 64;
+    if (N <= 128 || (split3 && !GEMM_SPLIT3_BN256)) return 128;
+    return 256;
+}
 
 }  // namespace
 
@@ -587,8 +638,10 @@ int gemm_tc_fwd(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, co
     CUtensorMap ta, tb;
     if (!make_map(&ta, A, M, K, lda, BK, BM, split3) || !make_map(&tb, Bt, N, K, ldb, BK, BN, split3))
         CDF_FAIL(CDFGNN_ECUDA, "cuTensorMapEncodeTiled failed (fwd)");
-    EpiArgs ep{C, ldc, nullptr, 0, nullptr, 0, 0};
-    return launch_bn<false, false>(BN, split3, ta, tb, M, N, K, 1, ep, s);
+    EpiArgs ep{C, ldc, nullptr, 0, nullptr, 0, 0, 0};
+    CUtensorMap tc;
+    ep.tma = make_store_map(&tc, C, M, ldc, ldc, 1, false) ? 1 : 0;
+    return launch_bn<false, false>(BN, split3, ta, tb, tc, M, N, K, 1, ep, s);
 }
 
 // C[M x ldc] = (A[M x K] (lda) · Bᵀ) ⊙ 𝟙[mask > 0], B given as [N x K] (row stride ldb, K-major)
@@ -598,8 +651,10 @@ int gemm_tc_bwd_data(int64_t M, int64_t N, int64_t K, const float* A, int64_t ld
     CUtensorMap ta, tb;
     if (!make_map(&ta, A, M, K, lda, BK, BM, split3) || !make_map(&tb, Bk, N, K, ldb, BK, BN, split3))
         CDF_FAIL(CDFGNN_ECUDA, "cuTensorMapEncodeTiled failed (bwd data)");
-    EpiArgs ep{C, ldc, mask, ldm, nullptr, 0, 0};
-    return launch_bn<false, false>(BN, split3, ta, tb, M, N, K, 1, ep, s);
+    EpiArgs ep{C, ldc, mask, ldm, nullptr, 0, 0, 0};
+    CUtensorMap tc;
+    ep.tma = (!mask || (ldm & 3) == 0) && make_store_map(&tc, C, M, ldc, ldc, 1, false) ? 1 : 0;
+    return launch_bn<false, false>(BN, split3, ta, tb, tc, M, N, K, 1, ep, s);
 }
 
 // C[M x N] (+)= Ht · Stᵀ with Ht = Hᵀ [M x K] (ldh) and St = Sᵀ [N x K] (lds), K = vertices; split-K
@@ -617,8 +672,10 @@ int gemm_tc_wgrad(int64_t M, int64_t N, int64_t K, const float* Ht, int64_t ldh,
     while (splits > 1 && splits * M * ldw > ws_cap) splits--;
     const int kbps = (int)((total_kb + splits - 1) / splits);
     const int zs = (int)((total_kb + kbps - 1) / kbps);
-    EpiArgs ep{nullptr, 0, nullptr, 0, ws, ldw, 0};
-    int rc = launch_bn<false, false>(BN, split3, ta, tb, M, N, K, (int)splits, ep, s);
+    EpiArgs ep{nullptr, 0, nullptr, 0, ws, ldw, 0, 0};
+    CUtensorMap tc;
+    ep.tma = make_store_map(&tc, ws, M, ldw, ldw, zs, true) ? 1 : 0;
+    int rc = launch_bn<false, false>(BN, split3, ta, tb, tc, M, N, K, (int)splits, ep, s);
     if (rc != CDFGNN_OK) CDF_FAIL(rc, "wgrad launch failed");
     const int64_t tot = M * ldc;
     splitk_sum_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(M, N, ldw, zs, ws, C, ldc, accumulate ? 1 : 0);

@@ -1,4 +1,4 @@
-// Which fp32 -> tf32 conversion does the TFLOAT32 tensor map apply?  (debug only)
+// Which fp32 -> tf32 conversion does kind::tf32 apply to RAW fp32 operands (FLOAT32 tensor map)?  (debug only)
 #include "../paper_2408_00232_b200/csrc/gemm_tc.cu"
 #include <cstdio>
 #include <vector>
@@ -16,7 +16,12 @@ int main() {
     for (auto& x : A) x = nd(g); for (auto& x : Bt) x = nd(g);
     float *dA, *dB, *dC; cudaMalloc(&dA, A.size()*4); cudaMalloc(&dB, Bt.size()*4); cudaMalloc(&dC, C.size()*4);
     cudaMemcpy(dA, A.data(), A.size()*4, cudaMemcpyHostToDevice); cudaMemcpy(dB, Bt.data(), Bt.size()*4, cudaMemcpyHostToDevice);
-    gemm_tc_fwd(M, N, K, dA, K, dB, K, dC, N, SPLIT, 0); cudaDeviceSynchronize();
+    CUtensorMap ta, tb;
+    if (!make_map(&ta, dA, M, K, K, BK, BM, true) || !make_map(&tb, dB, N, K, K, BK, 64, true)) { printf("map fail\n"); return 1; }
+    EpiArgs ep{dC, N, nullptr, 0, nullptr, 0, 0, 0};
+    CUtensorMap tc;
+    int rc = launch_bn<false, false>(64, false, ta, tb, tc, M, N, K, 1, ep, 0); cudaDeviceSynchronize();
+    printf("rc %d err %s\n", rc, cudaGetErrorString(cudaGetLastError()));
     cudaMemcpy(C.data(), dC, C.size()*4, cudaMemcpyDeviceToHost);
     double e[4] = {0,0,0,0};
     for (int m = 0; m < M; ++m) for (int n = 0; n < N; ++n) {
