@@ -265,6 +265,15 @@ int cdfgnn_epoch_host(cdfgnn_ctx* ctx, const float* const* X_host,
  *        4 master view b.  Device pointer into the workspace. */
 int cdfgnn_cache_view(cdfgnn_ctx* ctx, int32_t local_part, int32_t l, int32_t dir,
                       int32_t which, float** ptr, int64_t* rows, int64_t* ld);
+/* Activations and parameter gradients of the most recent cdfgnn_epoch (device pointers into
+ * the workspace, valid until the next call that runs layers):
+ *   cdfgnn_act_view:  H^(l) = σ(Z^(l)) of local part `local_part` for l < L, the logits
+ *                     Z^(L) for l = L (eqs. 1-2); rows = n_local, row stride ld(F_l),
+ *                     local row order (R21).
+ *   cdfgnn_grad_view: ∇W^(l-1) summed over all parts and ranks (Alg. 1 L12), the
+ *                     value the optimizer consumed; [F_{l-1} x F_l] row-major (ld = F_l). */
+int cdfgnn_act_view(cdfgnn_ctx* ctx, int32_t local_part, int32_t l, float** ptr, int64_t* rows, int64_t* ld);
+int cdfgnn_grad_view(cdfgnn_ctx* ctx, int32_t l, float** ptr, int64_t* rows, int64_t* ld);
 /* which: 0 gather-sent flag per mirror row, 1 master-fired flag, 2 active flag
  * (uint8 per row, of the most recent synchronisation). */
 int cdfgnn_sync_flags(cdfgnn_ctx* ctx, int32_t local_part, int32_t which, uint8_t** ptr,

@@ -30,6 +30,18 @@ def forward(A, X, W):
     return Z, H
 
 
+def rows_forward(A, H, W, rows):
+    """Z[v] = Σ_u Â[v,u] (H[u] W) for the listed rows only, one row at a time (eq. 1,
+    P:L237) — the plain definition evaluated for sampled outputs of a full-size graph."""
+    A = A.tocsr()
+    out = np.zeros((len(rows), W.shape[1]))
+    for i, v in enumerate(rows):
+        lo, hi = A.indptr[v], A.indptr[v + 1]
+        nb = A.indices[lo:hi]
+        out[i] = A.data[lo:hi] @ (H[nb] @ W)
+    return out
+
+
 def log_softmax(z):
     mx = z.max(axis=1, keepdims=True)
     sh = z - mx

@@ -120,6 +120,8 @@ _sig("cdfgnn_epoch_host", c_i32, [c_void_p, P(c_void_p), P(c_void_p), P(c_void_p
 _sig("cdfgnn_cache_view", c_i32, [c_void_p, c_i32, c_i32, c_i32, c_i32, P(c_void_p), P(c_i64),
                                   P(c_i64)])
 _sig("cdfgnn_sync_flags", c_i32, [c_void_p, c_i32, c_i32, P(c_void_p), P(c_i64)])
+_sig("cdfgnn_act_view", c_i32, [c_void_p, c_i32, c_i32, P(c_void_p), P(c_i64), P(c_i64)])
+_sig("cdfgnn_grad_view", c_i32, [c_void_p, c_i32, P(c_void_p), P(c_i64), P(c_i64)])
 _sig("cdfgnn_reset_caches", c_i32, [c_void_p, c_void_p])
 _sig("cdfgnn_get_eps", c_i32, [c_void_p, P(c_f64), P(c_f64)])
 _sig("cdfgnn_set_eps", c_i32, [c_void_p, c_f64])

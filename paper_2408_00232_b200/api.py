@@ -257,6 +257,24 @@ def cache_view(ctx: Ctx, local_part: int, l: int, direction: int, which: int):
     return p.value, rows.value, ld.value
 
 
+def act_view(ctx: Ctx, local_part: int, l: int):
+    """(device pointer, rows, ld) of H^(l) (l < L) or the logits (l = L) of the last epoch."""
+    p = ctypes.c_void_p()
+    rows = L.c_i64()
+    ld = L.c_i64()
+    check(_c.cdfgnn_act_view(ctx.handle, local_part, l, ctypes.byref(p), ctypes.byref(rows), ctypes.byref(ld)))
+    return p.value, rows.value, ld.value
+
+
+def grad_view(ctx: Ctx, l: int):
+    """(device pointer, rows, ld) of ∇W^(l-1) of the last epoch."""
+    p = ctypes.c_void_p()
+    rows = L.c_i64()
+    ld = L.c_i64()
+    check(_c.cdfgnn_grad_view(ctx.handle, l, ctypes.byref(p), ctypes.byref(rows), ctypes.byref(ld)))
+    return p.value, rows.value, ld.value
+
+
 def sync_flags(ctx: Ctx, local_part: int, which: int):
     p = ctypes.c_void_p()
     rows = L.c_i64()

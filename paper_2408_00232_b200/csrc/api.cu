@@ -1374,6 +1374,25 @@ extern "C" int cdfgnn_cache_view(cdfgnn_ctx* c, int32_t lp, int32_t l, int32_t d
     return CDFGNN_OK;
 }
 
+extern "C" int cdfgnn_act_view(cdfgnn_ctx* c, int32_t lp, int32_t l, float** ptr, int64_t* rows, int64_t* ld) {
+    if (!c || !ptr || !rows || !ld) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+    if (lp < 0 || lp >= c->k || l < 1 || l > c->cfg.L) CDF_FAIL(CDFGNN_EUSAGE, "bad part/layer");
+    const LocalPart& P = c->parts[lp];
+    *ptr = P.act[l];
+    *rows = P.n;
+    *ld = ld_of(c->cfg.dims[l]);
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_grad_view(cdfgnn_ctx* c, int32_t l, float** ptr, int64_t* rows, int64_t* ld) {
+    if (!c || !ptr || !rows || !ld) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+    if (l < 1 || l > c->cfg.L) CDF_FAIL(CDFGNN_EUSAGE, "bad layer");
+    *ptr = c->dW + c->woff[l - 1];
+    *rows = c->cfg.dims[l - 1];
+    *ld = c->cfg.dims[l];
+    return CDFGNN_OK;
+}
+
 extern "C" int cdfgnn_sync_flags(cdfgnn_ctx* c, int32_t lp, int32_t which, uint8_t** ptr, int64_t* rows) {
     if (!c || !ptr || !rows) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
     if (lp < 0 || lp >= c->k) CDF_FAIL(CDFGNN_EUSAGE, "bad part");

@@ -26,7 +26,24 @@ def test_two_gpus_match_one_gpu(mode, transport, overlap):
            "--master-addr", "127.0.0.1", "--master-port", "29517",
            os.path.join(ROOT, "tools", "mgpu_check.py"), "--mode", mode, "--epochs", "4",
            "--transport", transport, "--overlap", str(overlap)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert json.loads(lines[-1])["mgpu_check"] == "PASS"
+
+
+def test_two_gpus_full_size_C3_match_unpartitioned():
+    """The bench workload at full size on 2 GPUs (NVLink push), exact mode (ε = 0, fp32
+    messages): per-epoch loss and W equal the unpartitioned p = 1 model's (P-C1) and the
+    co-resident 2-part run's, and W is bit-identical on both ranks."""
+    torch = require_gpu()
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29518",
+           os.path.join(ROOT, "tools", "mgpu_check.py"), "--config", "C3", "--mode", "exact", "--epochs", "2",
+           "--vs-p1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert json.loads(lines[-1])["mgpu_check"] == "PASS"

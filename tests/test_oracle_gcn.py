@@ -36,6 +36,18 @@ def test_forward_dense_brute_force():
     np.testing.assert_allclose(Z[1], Z2, rtol=1e-12, atol=1e-12)
 
 
+def test_rows_forward_dense_brute_force():
+    """oracle.gcn.rows_forward (sampled rows of eq. 1) vs explicit loops on the dense Â."""
+    d = small_random_graph(30, 70, (6, 5, 3), seed=8)
+    A = normalized_adjacency(d.n, d.eu, d.ev)
+    X = d.X.astype(np.float64)
+    W = d.W[0].astype(np.float64)
+    rows = [0, 7, 29, 13, 7]
+    got = gcn.rows_forward(A, X, W, rows)
+    ref = _dense_loops(A.toarray(), X, W)[rows]
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+
+
 def _torch_ref(A, X, W, y, train):
     At = torch.tensor(A.toarray(), dtype=torch.float64)
     Wt = [torch.tensor(w, dtype=torch.float64, requires_grad=True) for w in W]

@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--mode", default="cache_int8")
     ap.add_argument("--transport", default="push")
     ap.add_argument("--overlap", type=int, default=0)
+    ap.add_argument("--vs-p1", action="store_true",
+                    help="rank 0 also runs the unpartitioned p = 1 model (exact mode: P-C1 at full size)")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -34,17 +36,25 @@ def main():
     from paper_2408_00232_b200.runtime import Run
     from synth import get_config, make_dataset, small_random_graph
     if a.config:
-        ds = make_dataset(get_config(a.config))
+        from synth.cache import cached_dataset
+        if rank == 0:
+            ds = cached_dataset(get_config(a.config))
+        dist.barrier()
+        if rank != 0:
+            ds = cached_dataset(get_config(a.config), wait_for_writer=True, write=False)
     else:
         ds = small_random_graph(3000, 20000, (24, 32, 6), seed=71)
     cache, quant = {"cache_int8": (True, 8), "cache_fp32": (True, 0), "nocache": (False, 0),
                     "exact": (True, 0)}[a.mode]
     eps0 = 0.0 if a.mode == "exact" else 0.01
+    # SGD when comparing with the unpartitioned model: Adam's first steps amplify rounding-level
+    # differences of near-zero gradients into ±lr moves, SGD keeps W linear in ∇W
     kw = dict(cache=cache, quant_bits=quant, eps0=eps0, adaptive=a.mode != "exact",
-              optimizer="adam", lr=0.01)
+              optimizer="sgd" if a.vs_p1 else "adam", lr=0.01)
     run = Run(ds, world, rank=rank, world=world, device=local, transport=a.transport,
               overlap=bool(a.overlap), **kw)
     ref = Run(ds, world, device=local, plan=run.plan, **kw) if rank == 0 else None
+    one = Run(ds, 1, device=local, **kw) if (rank == 0 and a.vs_p1) else None
     ok = True
     rows = []
     for ep in range(a.epochs):
@@ -64,6 +74,15 @@ def main():
             row = dict(epoch=ep, loss=g["loss"], loss_1gpu=r["loss"], rel=rel, w_same=bool(same),
                        msgs=int(sent.item()), msgs_1gpu=rsent, eps=g["eps_used"],
                        wire=sum(s["bytes_wire"] for s in g["fwd"] + g["bwd"]))
+            if one is not None:
+                o = one.epoch()
+                row["loss_p1"] = o["loss"]
+                row["rel_p1"] = abs(g["loss"] - o["loss"]) / max(1.0, abs(o["loss"]))
+                wd = max(float(np.abs(x.cpu().numpy() - y.cpu().numpy()).max() / max(np.abs(y.cpu().numpy()).max(), 1e-30))
+                         for x, y in zip(run.W, one.W))
+                row["w_rel_p1"] = wd
+                if row["rel_p1"] > 1e-5 or wd > 1e-4:
+                    ok = False
             rows.append(row)
             print(json.dumps(row), flush=True)
             tol = 1e-5 if a.mode == "exact" else 2e-3
@@ -77,6 +96,8 @@ def main():
     run.close()
     if ref:
         ref.close()
+    if one:
+        one.close()
     dist.barrier()
     dist.destroy_process_group()
     return 0 if ok else 1
