@@ -155,7 +155,13 @@ typedef struct {
                                            results: mirrors never read logits and their δ̈^(L) = 0) */
     int32_t static_inputs;              /* 1: the input features X do not change between calls for
                                            a given buffer, so Xᵀ (∇W^(0) operand) is built once per
-                                           X pointer and reused; 0 (default): rebuilt every epoch */
+                                           X pointer and reused; 0 (default): rebuilt every epoch;
+                                           2: also hoist the layer-1 aggregation — Â_i X_i is built
+                                           once per X pointer, layer 1 runs (Â_i X_i) W^(0) and
+                                           ∇W^(0) = (Â_i X_i)ᵀ δ^(1) (associativity of eq. (1),
+                                           P:L236-238, and of P:L273-278 with Â_i symmetric): both
+                                           layer-1 SpMMs leave the epoch; results equal the
+                                           per-epoch schedule up to fp32 rounding order */
     int32_t overlap;                    /* 1: boundary-rows-first scheduling (§8 f1) — the SpMM
                                            (forward) or ∇H GEMM (backward, inside cdfgnn_epoch)
                                            produces the mirror rows first, their gather phase (test,

@@ -96,6 +96,8 @@ struct LocalPart {
     float* hT[CDFGNN_MAX_LAYERS] = {}; // H^(l)ᵀ written with the forward ReLU (epoch, tcgen05 path)
     const float* hT_src[CDFGNN_MAX_LAYERS] = {};   // the H^(l) buffer hT[l] mirrors
     const float* xT_src = nullptr;     // the X pointer xT was built from
+    float* ax = nullptr;               // cfg.static_inputs == 2: Â_i X_i, built once per X pointer
+    const float* ax_src = nullptr;     // (xT then holds (Â_i X_i)ᵀ)
     float* val = nullptr;
     int64_t *moff_d = nullptr, *hoff_d = nullptr;
     uint8_t* regA[kMaxParts] = {};
@@ -171,6 +173,11 @@ int64_t sync_width(const cdfgnn_ctx* c, int l) { return c->cfg.dims[l]; }
 // Else chunk > 0: rows longer than `chunk` neighbours become ceil(deg/chunk) chunks and
 // every item is visited longest first.  items2_h holds the same items with the mirror
 // rows' first (boundary-rows-first scheduling, §8 f1), order otherwise kept.
+int env_knob(const char* name, int dflt) {
+    const char* e = getenv(name);    // tuning knobs for tools/spmm_bench.py
+    return e ? atoi(e) : dflt;
+}
+
 void build_spmm_items(const LocalPart& P, SpmmPlan& S, int chunk, int phases, int min_deg) {
     S.split_h.assign(P.n, make_int4(-1, 0, 0, 0));
     S.seg_beg_h.clear();
@@ -227,9 +234,20 @@ void build_spmm_items(const LocalPart& P, SpmmPlan& S, int chunk, int phases, in
                 w.push_back({deg, make_int2((int)r, -1)});
             }
         }
-        std::stable_sort(w.begin(), w.end(), [](const std::pair<int32_t, int2>& a, const std::pair<int32_t, int2>& b) {
+        // order: 0 = longest first (LPT); 1 = row order (locality of the local numbering);
+        // 2 = items longer than CDFGNN_SPMM_HEAVY neighbours longest first, then row order
+        const int order = env_knob("CDFGNN_SPMM_ORDER", 0);
+        auto by_weight = [](const std::pair<int32_t, int2>& a, const std::pair<int32_t, int2>& b) {
             return a.first > b.first;
-        });
+        };
+        if (order == 0) {
+            std::stable_sort(w.begin(), w.end(), by_weight);
+        } else if (order == 2) {
+            const int32_t heavy = env_knob("CDFGNN_SPMM_HEAVY", 4096);
+            auto mid = std::stable_partition(w.begin(), w.end(),
+                                             [&](const std::pair<int32_t, int2>& a) { return a.first > heavy; });
+            std::stable_sort(w.begin(), mid, by_weight);
+        }
     }
     if (S.seg_beg_h.empty()) S.seg_beg_h.push_back(0);
     S.n_items = (int64_t)w.size();
@@ -299,6 +317,7 @@ int prepare(cdfgnn_ctx* c, const cdfgnn_plan* plan, const int32_t* parts, int32_
     int64_t maxw = 0;
     for (int l = 1; l <= cfg->L; ++l) maxw = std::max<int64_t>(maxw, (int64_t)cfg->dims[l - 1] * cfg->dims[l]);
     c->splitk_cap = 64 * maxw;
+    if (c->cfg.static_inputs < 0 || c->cfg.static_inputs > 2) CDF_FAIL(CDFGNN_EUSAGE, "static_inputs must be 0, 1 or 2");
     c->parts.assign(k, LocalPart());
     for (int t = 0; t < k; ++t) {
         cdfgnn_part_view v;
@@ -325,7 +344,7 @@ int prepare(cdfgnn_ctx* c, const cdfgnn_plan* plan, const int32_t* parts, int32_
 }
 
 int64_t region_bytes(const cdfgnn_ctx* c, int64_t cap) {
-    const int64_t rowb = c->cfg.quant_bits ? c->Fmax : 4 * c->ldmax;
+    const int64_t rowb = c->cfg.quant_bits ? c->ldmax : 4 * c->ldmax;   // code rows: ld bytes
     return align_up(cap * c->hdr_bytes, 256) + cap * rowb;
 }
 
@@ -362,7 +381,7 @@ void carve(cdfgnn_ctx* c, Bump& b) {
         P.active = b.take<uint8_t>(P.B);
         P.idxmap = b.take<int32_t>((int64_t)p * P.B);
         P.mmap = b.take<int32_t>(P.M);
-        P.stage_codes = b.take<uint8_t>(P.B * c->Fmax);
+        P.stage_codes = b.take<uint8_t>(P.B * c->ldmax);
         P.stage_lohi = b.take<float>(2 * P.B);
         P.stage_a = b.take<float>(P.B * c->ldmax);
         for (int l = 1; l <= L; ++l) {
@@ -387,6 +406,7 @@ void carve(cdfgnn_ctx* c, Bump& b) {
         P.D[1] = b.take<float>(P.n * c->ldmax);
         P.rowloss = b.take<float>(P.n);
         P.X_stage = b.take<float>(P.n * ld_of(c->cfg.dims[0]));
+        if (c->cfg.static_inputs == 2) P.ax = b.take<float>(P.n * ld_of(c->cfg.dims[0]));
         P.lab_stage = b.take<int32_t>(P.n);
         P.mask_stage = b.take<uint8_t>(P.n);
     }
@@ -658,7 +678,7 @@ int halo_gather(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, floa
     if (ld != ld_of(F)) CDF_FAIL(CDFGNN_EUSAGE, "ld %lld must equal roundup(F=%d, 4)", (long long)ld, F);
     std::vector<SyncArgs> args;
     sync_args(c, l, dir, X, ld, eps, false, args);
-    const int64_t rowb = c->cfg.quant_bits ? F : 4 * ld;
+    const int64_t rowb = c->cfg.quant_bits ? ld : 4 * ld;   // code rows padded to ld bytes
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
         const int nt = gather_tiles_host(P.moff.data(), p, ld);
@@ -685,7 +705,7 @@ int halo_finish(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, floa
     const int F = (int)sync_width(c, l);
     std::vector<SyncArgs> args;
     sync_args(c, l, dir, X, ld, eps, skip_gather, args);
-    const int64_t rowb = c->cfg.quant_bits ? F : 4 * ld;
+    const int64_t rowb = c->cfg.quant_bits ? ld : 4 * ld;   // code rows padded to ld bytes
     mark(c, PH_SYNC, s, SS_MASTER);
     // ---- masters: apply in ascending source order, own test, stage scatter (L10-L19)
     for (int t = 0; t < c->k; ++t) {
@@ -693,9 +713,9 @@ int halo_finish(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, floa
         if (P.B == 0) continue;
         if (!skip_gather) {
             CUDA_TRY(cudaMemsetAsync(P.idxmap, 0xFF, sizeof(int32_t) * p * P.B, s));
-            c->launches += launch_map(P.halo, 0, *std::max_element(P.capB.begin(), P.capB.end()), s);
+            c->launches += launch_map(P.halo, P.grecv_h, 0, *std::max_element(P.capB.begin(), P.capB.end()), s);
         }
-        c->launches += launch_master(P.halo, args[t], s);
+        c->launches += launch_master(P.halo, args[t], P.grecv_h, s);
     }
     CDF_TRY(check_launch("master"));
     if (skip_scatter) return CDFGNN_OK;
@@ -722,8 +742,8 @@ int halo_finish(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, floa
         LocalPart& P = c->parts[t];
         if (P.M == 0) continue;
         CUDA_TRY(cudaMemsetAsync(P.mmap, 0xFF, sizeof(int32_t) * P.M, s));
-        c->launches += launch_map(P.halo, 1, *std::max_element(P.capA.begin(), P.capA.end()), s);
-        c->launches += launch_mirror_apply(P.halo, args[t], s);
+        c->launches += launch_map(P.halo, P.srecv_h, 1, *std::max_element(P.capA.begin(), P.capA.end()), s);
+        c->launches += launch_mirror_apply(P.halo, args[t], P.srecv_h, s);
     }
     CDF_TRY(check_launch("mirror_apply"));
     return CDFGNN_OK;
@@ -782,7 +802,7 @@ void fill_sync_stats(const cdfgnn_ctx* c, int l, int dir, const unsigned long lo
     st->bytes_alg = (h[0] + h[3]) * mb;
     st->bytes_wire = wire;
     if (c->transport == 2)      // NVLink push: every message is stored into a peer GPU
-        st->bytes_wire = (int64_t)(h[0] + h[3]) * (c->hdr_bytes + (c->cfg.quant_bits ? F : 4 * ld_of(F)));
+        st->bytes_wire = (int64_t)(h[0] + h[3]) * (c->hdr_bytes + (c->cfg.quant_bits ? ld_of(F) : 4 * ld_of(F)));
     (void)dir;
 }
 
@@ -807,6 +827,33 @@ int spmm_part(cdfgnn_ctx* c, LocalPart& P, const float* T, float* Y, int64_t ld,
     return check_launch("spmm");
 }
 
+// cfg.static_inputs == 2 (hoisted input aggregation): X is fixed per buffer, so the
+// layer-1 product Â_i X_i W^(0) of eq. (1) is evaluated as (Â_i X_i) W^(0) with Â_i X_i
+// aggregated once per X pointer (associativity), and ∇W^(0) = X_iᵀ (Â_i δ^(1))
+// (reading R6) as (Â_i X_i)ᵀ δ^(1) (Â_i symmetric) — both layer-1 SpMMs leave
+// the epoch.  Results agree with the per-epoch schedule up to fp32 rounding order.
+bool hoisted(const cdfgnn_ctx* c, int l) { return l == 1 && c->cfg.static_inputs == 2; }
+
+int ensure_ax(cdfgnn_ctx* c, LocalPart& P, const float* X, int64_t ld_in, cudaStream_t s) {
+    if (P.ax_src == X) return CDFGNN_OK;
+    const int64_t F0 = c->cfg.dims[0];
+    if (ld_in != ld_of(F0)) CDF_FAIL(CDFGNN_EUSAGE, "hoisted input aggregation needs ld(X) = %lld",
+                                     (long long)ld_of(F0));
+    const SpmmPlan& S = spmm_plan(P, ld_in);
+    if (S.nslots && ld_in > S.pstride) CDF_FAIL(CDFGNN_EUSAGE, "split SpMM rows cannot hold ld %lld",
+                                                (long long)ld_in);
+    mark(c, PH_OTHER, s);
+    launch_spmm(P.rowptr, P.colidx, P.val, S.n_items, spmm_items(P, 0, ld_in), X, P.ax, ld_in, s);
+    c->launches++;
+    CDF_TRY(check_launch("spmm (input aggregation)"));
+    if (P.xT) {
+        c->launches += launch_transpose(P.ax, P.n, F0, ld_in, P.xT, ld_of(P.n), s);
+        P.xT_src = P.ax;
+    }
+    P.ax_src = X;
+    return CDFGNN_OK;
+}
+
 int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, const float* W,
              float* const* Z, float* const* H_out, int64_t ld_out, float eps, cudaStream_t s,
              int64_t* wire, bool elide = false) {
@@ -814,23 +861,30 @@ int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, cons
     if (ld_in < Fi || ld_in % 4 || ld_out != ld_of(Fo)) CDF_FAIL(CDFGNN_EUSAGE, "bad leading dimension");
     float* Wt = c->wtpad + c->wtoff[l - 1];
     const int64_t ldwt = ld_of(Fi);
-    const bool ov = overlap_on(c);
+    const bool hz = hoisted(c, l);
+    const bool ov = overlap_on(c) && !hz;
     if (c->cfg.gemm_tf32) {
         mark(c, PH_GEMM, s);
         c->launches += launch_transpose(W, Fi, Fo, Fo, Wt, ldwt, s);
     }
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
+        const float* A = H_in[t];
+        if (hz) {
+            CDF_TRY(ensure_ax(c, P, H_in[t], ld_in, s));
+            A = P.ax;
+        }
+        float* out = hz ? Z[t] : P.T;      // hoisted: the GEMM yields Z̈ directly
         mark(c, PH_GEMM, s);
         if (c->cfg.gemm_tf32) {
-            CDF_TRY(gemm_tc_fwd(P.n, Fo, Fi, H_in[t], ld_in, Wt, ldwt, P.T, ld_out, c->cfg.gemm_tf32 == 3, s));
+            CDF_TRY(gemm_tc_fwd(P.n, Fo, Fi, A, ld_in, Wt, ldwt, out, ld_out, c->cfg.gemm_tf32 == 3, s));
         } else {
-            launch_gemm_simt(false, false, P.n, Fo, Fi, H_in[t], ld_in, W, Fo, P.T, ld_out, nullptr, 0,
+            launch_gemm_simt(false, false, P.n, Fo, Fi, A, ld_in, W, Fo, out, ld_out, nullptr, 0,
                              nullptr, 0, false, s);
         }
         c->launches++;
         CDF_TRY(check_launch("gemm fwd"));
-        CDF_TRY(spmm_part(c, P, P.T, Z[t], ld_out, s, ov ? 1 : 0));
+        if (!hz) CDF_TRY(spmm_part(c, P, P.T, Z[t], ld_out, s, ov ? 1 : 0));
     }
     if (ov) {
         // §8 f1: the mirror rows are done — their gather runs on s2 under the remaining SpMM rows
@@ -884,8 +938,13 @@ int bwd_impl(cdfgnn_ctx* c, int l, float* const* dZ, int64_t ld, const float* co
         c->launches++;
         return check_launch("gemm bwd_data");
     };
+    const bool hz = hoisted(c, l);
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
+        if (hz) {
+            CDF_TRY(ensure_ax(c, P, H_in[t], ld_in, s));   // no SpMM: ∇W^(0) = (Â_i X_i)ᵀ δ^(1)
+            continue;
+        }
         CDF_TRY(spmm_part(c, P, dZ[t], P.S, ld, s));
         mark(c, PH_GEMM, s);
         if (c->cfg.gemm_tf32 && t == 0)
@@ -897,10 +956,17 @@ int bwd_impl(cdfgnn_ctx* c, int l, float* const* dZ, int64_t ld, const float* co
         LocalPart& P = c->parts[t];
         mark(c, PH_GEMM, s);
         // dW (+)= H_inᵀ S ; parts accumulate in ascending order
+        const float* Sg = hz ? dZ[t] : P.S;      // hoisted layer 1: (Â_i X_i)ᵀ δ^(1)
+        const float* Hg = hz ? P.ax : H_in[t];
         if (c->cfg.gemm_tf32) {
             const float* Ht = c->trA;
             int64_t ldh = c->npad;
-            if (l == 1 && P.xT) {
+            if (hz && P.xT) {
+                Ht = P.xT;                      // (Â_i X_i)ᵀ, built by ensure_ax
+                ldh = ld_of(P.n);
+            } else if (hz) {
+                c->launches += launch_transpose(P.ax, P.n, Fi, ld_in, c->trA, c->npad, s);
+            } else if (l == 1 && P.xT) {
                 // static inputs: H^(0)ᵀ = Xᵀ is transposed once per X buffer and reused
                 if (P.xT_src != H_in[t]) {
                     c->launches += launch_transpose(H_in[t], P.n, Fi, ld_in, P.xT, ld_of(P.n), s);
@@ -914,11 +980,11 @@ int bwd_impl(cdfgnn_ctx* c, int l, float* const* dZ, int64_t ld, const float* co
             } else {
                 c->launches += launch_transpose(H_in[t], P.n, Fi, ld_in, c->trA, c->npad, s);
             }
-            c->launches += launch_transpose(P.S, P.n, Fo, ld, c->trB, c->npad, s);
+            c->launches += launch_transpose(Sg, P.n, Fo, ld, c->trB, c->npad, s);
             CDF_TRY(gemm_tc_wgrad(Fi, Fo, P.n, Ht, ldh, c->trB, c->npad, dW, Fo, c->splitk,
                                   c->splitk_cap, t > 0, c->cfg.gemm_tf32 == 3, s, &c->launches));
         } else {
-            launch_gemm_simt(true, false, Fi, Fo, P.n, H_in[t], ld_in, P.S, ld, dW, Fo, nullptr, 0,
+            launch_gemm_simt(true, false, Fi, Fo, P.n, Hg, ld_in, Sg, ld, dW, Fo, nullptr, 0,
                              c->splitk, c->splitk_cap, t > 0, s);
             c->launches += 2;
         }

@@ -85,10 +85,12 @@ int gather_tiles_host(const int64_t* moff, int p, int64_t ld);
 int scatter_tiles_host(const int64_t* hoff, int p);
 // Each launcher returns the number of kernels it launched.
 int launch_gather_pack_n(const HaloDev& h, const SyncArgs& a, int ntiles, cudaStream_t s);
-int launch_map(const HaloDev& h, int mirror_side, int64_t max_count, cudaStream_t s);
-int launch_master(const HaloDev& h, const SyncArgs& a, cudaStream_t s);
+// rt: the receive-side region table (host copy, passed by value as a kernel parameter so the
+// message pointers need no dependent global load)
+int launch_map(const HaloDev& h, const RegionTab& rt, int mirror_side, int64_t max_count, cudaStream_t s);
+int launch_master(const HaloDev& h, const SyncArgs& a, const RegionTab& rt, cudaStream_t s);
 int launch_scatter_pack_n(const HaloDev& h, const SyncArgs& a, int ntiles, cudaStream_t s);
-int launch_mirror_apply(const HaloDev& h, const SyncArgs& a, cudaStream_t s);
+int launch_mirror_apply(const HaloDev& h, const SyncArgs& a, const RegionTab& rt, cudaStream_t s);
 
 // ---- SpMM (kernels_spmm.cu): Y[n x ld] = Â T
 // Work items in visiting order: {row, seg} (seg = -1: the whole row; else segment seg of a

@@ -47,25 +47,18 @@ __device__ __forceinline__ float step8(float lo, float hi) {
     return __fmul_rn(__fsub_rn(hi, lo), 0.00390625f);   // RN((hi−lo)·2^-8)
 }
 
-// 4 consecutive uint8 codes at column c0 of an F-wide code row (one 32-bit access when the
-// row is 4-byte aligned, i.e. F % 4 == 0; out-of-range columns read as 0 / are not written)
-__device__ __forceinline__ void load_codes4(const uint8_t* row, int c0, int F, uint32_t (&q)[4]) {
-    if ((F & 3) == 0 && c0 + 3 < F) {
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(row + c0);
-        q[0] = w & 0xFFu; q[1] = (w >> 8) & 0xFFu; q[2] = (w >> 16) & 0xFFu; q[3] = w >> 24;
-    } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) q[k] = c0 + k < F ? row[c0 + k] : 0u;
-    }
+// 4 consecutive uint8 codes at column c0 of a code row.  Code rows are ld = roundup(F, 4)
+// bytes long (padding codes are 0), so every group of 4 is one aligned 32-bit access.
+__device__ __forceinline__ void load_codes4(const uint8_t* row, int c0, uint32_t (&q)[4]) {
+    const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(row + c0));
+    q[0] = w & 0xFFu; q[1] = (w >> 8) & 0xFFu; q[2] = (w >> 16) & 0xFFu; q[3] = w >> 24;
 }
 __device__ __forceinline__ void store_codes4(uint8_t* row, int c0, int F, const uint32_t (&q)[4]) {
-    if ((F & 3) == 0 && c0 + 3 < F) {
-        *reinterpret_cast<uint32_t*>(row + c0) = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
-    } else {
+    uint32_t w = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (c0 + k < F) row[c0 + k] = (uint8_t)q[k];
-    }
+    for (int k = 0; k < 4; ++k)
+        if (c0 + k < F) w |= q[k] << (8 * k);
+    *reinterpret_cast<uint32_t*>(row + c0) = w;
 }
 
 template <int LPR>
@@ -200,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 3 : 1) gather_pack_kernel
                 hp[1] = __float_as_uint(lo[r]);
                 hp[2] = __float_as_uint(hi[r]);
             }
-            uint8_t* codes = pay + mm * (int64_t)a.F;
+            uint8_t* codes = pay + mm * a.ld;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
@@ -237,12 +230,11 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 3 : 1) gather_pack_kernel
 // map: message -> row tables.  mirror_side = 0: idxmap[src*B + master row] = m;
 // mirror_side = 1: mmap[mirror index] = m.
 // ==================================================================================
-__global__ void map_kernel(HaloDev h, int mirror_side) {
+__global__ void map_kernel(HaloDev h, const __grid_constant__ RegionTab t, int mirror_side) {
     const int q = blockIdx.y;
     if (q == h.me) return;
-    const RegionTab* t = mirror_side ? h.srecv : h.grecv;
-    const int32_t cnt = *t->cnt[q];
-    const uint8_t* hdr = t->hdr[q];
+    const int32_t cnt = *t.cnt[q];
+    const uint8_t* hdr = t.hdr[q];
     const int64_t len = mirror_side ? (h.moff[q + 1] - h.moff[q]) : (h.hoff[q + 1] - h.hoff[q]);
     if (cnt > len) { if (threadIdx.x == 0 && blockIdx.x == 0) atomicExch(h.err, 1); return; }
     for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < cnt;
@@ -258,7 +250,8 @@ __global__ void map_kernel(HaloDev h, int mirror_side) {
 // master: one row group per boundary master row
 // ==================================================================================
 template <int LPR, int VPL>
-__global__ void __launch_bounds__(kThreads, VPL <= 2 ? 4 : 1) master_kernel(HaloDev h, SyncArgs a) {
+__global__ void __launch_bounds__(kThreads, VPL <= 2 ? 4 : 1) master_kernel(HaloDev h, SyncArgs a,
+                                                                             const __grid_constant__ RegionTab rt) {
     constexpr int GPW = 32 / LPR;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane / LPR, gl = lane % LPR;
@@ -290,9 +283,9 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 4 : 1) master_kernel(Halo
         if (valid && gl < nsrc && gl != h.me) {
             mine = h.idxmap[(int64_t)gl * h.B + r];
             if (mine >= 0 && h.quant) {
-                const uint32_t* hp = reinterpret_cast<const uint32_t*>(h.grecv->hdr[gl] + (int64_t)mine * 12);
-                mlo = __uint_as_float(hp[1]);
-                mhi = __uint_as_float(hp[2]);
+                const uint32_t* hp = reinterpret_cast<const uint32_t*>(rt.hdr[gl] + (int64_t)mine * 12);
+                mlo = __uint_as_float(__ldg(hp + 1));
+                mhi = __uint_as_float(__ldg(hp + 2));
             }
         }
     }
@@ -313,22 +306,22 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 4 : 1) master_kernel(Halo
             m = valid ? h.idxmap[(int64_t)s * h.B + r] : -1;
             if (m < 0) continue;
             if (h.quant) {
-                const uint32_t* hp = reinterpret_cast<const uint32_t*>(h.grecv->hdr[s] + (int64_t)m * 12);
+                const uint32_t* hp = reinterpret_cast<const uint32_t*>(rt.hdr[s] + (int64_t)m * 12);
                 lo = __uint_as_float(hp[1]);
                 hi = __uint_as_float(hp[2]);
             }
         }
         any_msg = true;
-        const uint8_t* pay = h.grecv->pay[s];
+        const uint8_t* pay = rt.pay[s];
         if (h.quant) {
             const float stp = step8(lo, hi);
-            const uint8_t* codes = pay + (int64_t)m * a.F;
+            const uint8_t* codes = pay + (int64_t)m * a.ld;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
                 if (c0 >= a.F) continue;
                 uint32_t q[4];
-                load_codes4(codes, c0, a.F, q);
+                load_codes4(codes, c0, q);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     if (c0 + k < a.F)
@@ -406,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 4 : 1) master_kernel(Halo
     if (act) {
         if (h.quant) {
             const float rng = __fsub_rn(hi, lo), stp = step8(lo, hi);
-            uint8_t* codes = h.stage_codes + r * a.F;
+            uint8_t* codes = h.stage_codes + r * a.ld;
             if (gl == 0) { h.stage_lohi[2 * r] = lo; h.stage_lohi[2 * r + 1] = hi; }
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
@@ -512,22 +505,12 @@ __global__ void __launch_bounds__(kThreads) scatter_pack_kernel(HaloDev h, SyncA
     // payloads: the block's destination range is contiguous, so the copy is flattened over
     // (message, word) with coalesced stores
     if (h.quant) {
-        const int F = a.F;
-        if ((F & 3) == 0) {
-            const int wpr = F >> 2;
-            uint32_t* dst = reinterpret_cast<uint32_t*>(pay + m0 * (int64_t)F);
-            const int64_t nw = (int64_t)total * wpr;
-            for (int64_t i = threadIdx.x; i < nw; i += kThreads) {
-                const int k = (int)(i / wpr), o = (int)(i - (int64_t)k * wpr);
-                dst[i] = reinterpret_cast<const uint32_t*>(h.stage_codes + (int64_t)s_row[k] * F)[o];
-            }
-        } else {
-            uint8_t* dst = pay + m0 * (int64_t)F;
-            const int64_t nb = (int64_t)total * F;
-            for (int64_t i = threadIdx.x; i < nb; i += kThreads) {
-                const int k = (int)(i / F), o = (int)(i - (int64_t)k * F);
-                dst[i] = h.stage_codes[(int64_t)s_row[k] * F + o];
-            }
+        const int wpr = (int)(a.ld >> 2);        // code rows are ld bytes
+        uint32_t* dst = reinterpret_cast<uint32_t*>(pay + m0 * a.ld);
+        const int64_t nw = (int64_t)total * wpr;
+        for (int64_t i = threadIdx.x; i < nw; i += kThreads) {
+            const int k = (int)(i / wpr), o = (int)(i - (int64_t)k * wpr);
+            dst[i] = reinterpret_cast<const uint32_t*>(h.stage_codes + (int64_t)s_row[k] * a.ld)[o];
         }
     } else {
         const float* srcb = a.nocache ? h.stage_a : a.c.a;
@@ -546,7 +529,8 @@ __global__ void __launch_bounds__(kThreads) scatter_pack_kernel(HaloDev h, SyncA
 // mirror_apply: one row group per mirror row
 // ==================================================================================
 template <int LPR, int VPL>
-__global__ void __launch_bounds__(kThreads) mirror_apply_kernel(HaloDev h, SyncArgs a) {
+__global__ void __launch_bounds__(kThreads) mirror_apply_kernel(HaloDev h, SyncArgs a,
+                                                                const __grid_constant__ RegionTab rt) {
     constexpr int GPW = 32 / LPR;
     __shared__ int64_t s_moff[kMaxParts + 1];
     if (threadIdx.x <= h.p) s_moff[threadIdx.x] = h.moff[threadIdx.x];
@@ -565,19 +549,19 @@ __global__ void __launch_bounds__(kThreads) mirror_apply_kernel(HaloDev h, SyncA
         b[v] = (bmr && c0 < a.ld) ? ld4(bmr + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     if (m >= 0) {
-        const uint8_t* hdr = h.srecv->hdr[q];
-        const uint8_t* pay = h.srecv->pay[q];
+        const uint8_t* hdr = rt.hdr[q];
+        const uint8_t* pay = rt.pay[q];
         if (h.quant) {
             const uint32_t* hp = reinterpret_cast<const uint32_t*>(hdr + (int64_t)m * 12);
-            const float lo = __uint_as_float(hp[1]), hi = __uint_as_float(hp[2]);
+            const float lo = __uint_as_float(__ldg(hp + 1)), hi = __uint_as_float(__ldg(hp + 2));
             const float stp = step8(lo, hi);
-            const uint8_t* codes = pay + (int64_t)m * a.F;
+            const uint8_t* codes = pay + (int64_t)m * a.ld;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
                 if (c0 >= a.F) continue;
                 uint32_t q[4];
-                load_codes4(codes, c0, a.F, q);
+                load_codes4(codes, c0, q);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     if (c0 + k < a.F)
@@ -640,7 +624,7 @@ Shape shape_of(int64_t ld) {
     if (nv <= 2) return {2, 1};
     if (nv <= 4) return {4, 1};
     if (nv <= 8) return {8, 1};
-    if (nv <= 16) return {16, 1};
+    if (nv <= 16) return {8, 2};      // 4 rows per warp (ld 36..64; C3's 41 classes: 11 float4)
     if (nv <= 32) return {32, 1};
     if (nv <= 64) return {32, 2};
     if (nv <= 128) return {32, 4};
@@ -649,7 +633,7 @@ Shape shape_of(int64_t ld) {
 
 // rows per warp pass of gather_pack (must match the launch dispatch below)
 int gather_rpw(int lpr, int vpl) {
-    if (lpr == 16) return 2;
+    if (lpr == 16 || (lpr == 8 && vpl == 2)) return 2;
     if (lpr < 32) return 1;
     return vpl <= 2 ? 4 : (vpl == 4 ? 2 : 1);
 }
@@ -659,7 +643,8 @@ int gather_rpw(int lpr, int vpl) {
         Shape _s = shape_of(LD);                                                            \
         if (_s.lpr == 2) KERNEL<2, 1><<<GRID(2), kThreads, 0, STREAM>>>(__VA_ARGS__);       \
         else if (_s.lpr == 4) KERNEL<4, 1><<<GRID(4), kThreads, 0, STREAM>>>(__VA_ARGS__);  \
-        else if (_s.lpr == 8) KERNEL<8, 1><<<GRID(8), kThreads, 0, STREAM>>>(__VA_ARGS__);  \
+        else if (_s.lpr == 8 && _s.vpl == 1) KERNEL<8, 1><<<GRID(8), kThreads, 0, STREAM>>>(__VA_ARGS__); \
+        else if (_s.lpr == 8) KERNEL<8, 2><<<GRID(8), kThreads, 0, STREAM>>>(__VA_ARGS__);  \
         else if (_s.lpr == 16) KERNEL<16, 1><<<GRID(16), kThreads, 0, STREAM>>>(__VA_ARGS__); \
         else if (_s.vpl == 1) KERNEL<32, 1><<<GRID(32), kThreads, 0, STREAM>>>(__VA_ARGS__); \
         else if (_s.vpl == 2) KERNEL<32, 2><<<GRID(32), kThreads, 0, STREAM>>>(__VA_ARGS__); \
@@ -687,7 +672,8 @@ int launch_gather_pack_n(const HaloDev& h, const SyncArgs& a, int ntiles, cudaSt
     const Shape sh = shape_of(a.ld);
     if (sh.lpr == 2) gather_pack_kernel<2, 1, 1><<<ntiles, kThreads, 0, s>>>(h, a);
     else if (sh.lpr == 4) gather_pack_kernel<4, 1, 1><<<ntiles, kThreads, 0, s>>>(h, a);
-    else if (sh.lpr == 8) gather_pack_kernel<8, 1, 1><<<ntiles, kThreads, 0, s>>>(h, a);
+    else if (sh.lpr == 8 && sh.vpl == 1) gather_pack_kernel<8, 1, 1><<<ntiles, kThreads, 0, s>>>(h, a);
+    else if (sh.lpr == 8) gather_pack_kernel<8, 2, 2><<<ntiles, kThreads, 0, s>>>(h, a);
     else if (sh.lpr == 16) gather_pack_kernel<16, 1, 2><<<ntiles, kThreads, 0, s>>>(h, a);
     else if (sh.vpl == 1) gather_pack_kernel<32, 1, 4><<<ntiles, kThreads, 0, s>>>(h, a);
     else if (sh.vpl == 2) gather_pack_kernel<32, 2, 4><<<ntiles, kThreads, 0, s>>>(h, a);
@@ -705,20 +691,20 @@ int launch_put(const PutTab* tab, int p, int64_t hdr_bytes, int64_t row_bytes, i
     return 1;
 }
 
-int launch_map(const HaloDev& h, int mirror_side, int64_t max_count, cudaStream_t s) {
+int launch_map(const HaloDev& h, const RegionTab& rt, int mirror_side, int64_t max_count, cudaStream_t s) {
     if (max_count <= 0 || h.p <= 1) return 0;
     dim3 grid((unsigned)std::min<int64_t>((max_count + 255) / 256, 4096), h.p);
-    map_kernel<<<grid, 256, 0, s>>>(h, mirror_side);
+    map_kernel<<<grid, 256, 0, s>>>(h, rt, mirror_side);
     return 1;
 }
 
-int launch_master(const HaloDev& h, const SyncArgs& a, cudaStream_t s) {
+int launch_master(const HaloDev& h, const SyncArgs& a, const RegionTab& rt, cudaStream_t s) {
     if (h.B <= 0) return 0;
     auto grid = [&](int lpr) {
         const int64_t rows_per_block = kWarps * (32 / lpr);
         return (unsigned)((h.B + rows_per_block - 1) / rows_per_block);
     };
-    CDF_DISPATCH(a.ld, master_kernel, grid, s, h, a);
+    CDF_DISPATCH(a.ld, master_kernel, grid, s, h, a, rt);
     return 1;
 }
 
@@ -728,13 +714,13 @@ int launch_scatter_pack_n(const HaloDev& h, const SyncArgs& a, int ntiles, cudaS
     return 1;
 }
 
-int launch_mirror_apply(const HaloDev& h, const SyncArgs& a, cudaStream_t s) {
+int launch_mirror_apply(const HaloDev& h, const SyncArgs& a, const RegionTab& rt, cudaStream_t s) {
     if (h.M <= 0) return 0;
     auto grid = [&](int lpr) {
         const int64_t rows_per_block = kWarps * (32 / lpr);
         return (unsigned)((h.M + rows_per_block - 1) / rows_per_block);
     };
-    CDF_DISPATCH(a.ld, mirror_apply_kernel, grid, s, h, a);
+    CDF_DISPATCH(a.ld, mirror_apply_kernel, grid, s, h, a, rt);
     return 1;
 }
 

@@ -225,7 +225,14 @@ void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val,
     else if (nv <= 4) launch<4, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
     else if (nv <= 8) launch<8, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
     else if (nv <= 16) {
-        if (unr == 4) launch<16, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+        // 8 lanes x 2 float4 per row, 8 neighbours in flight, predicated tail batch: at ld = 44
+        // (C3's 41 classes) 1.75 -> 1.48 ms per launch vs 16 lanes x 1 (p = 1, tools/spmm_bench.py,
+        // profiles/r1); 4x3 and 2x6 were slower (fewer neighbours in flight per lane)
+        const int shape = env_int("CDFGNN_SPMM_SHAPE", 3);
+        if (shape == 1 && nv <= 12) launch<4, 3, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
+        else if (shape == 2 && nv <= 12) launch<2, 6, 2>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
+        else if (shape == 3) launch<8, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
+        else if (unr == 4) launch<16, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
         else launch<16, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
     } else if (nv <= 32) {
         if (unr == 4) launch<32, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);

@@ -33,7 +33,7 @@ class Run:
                  timing: bool = False, plan: Optional[api.Plan] = None,
                  host_inputs: bool = False, partition_kw: Optional[Dict] = None,
                  gemm: str = "tf32x3", transport: str = "push", elide: bool = True,
-                 static_inputs: bool = False, overlap: bool = False):
+                 static_inputs: int = 0, overlap: bool = False):
         import torch
         self.torch = torch
         self.ds = ds

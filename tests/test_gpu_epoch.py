@@ -161,3 +161,26 @@ def test_dead_sync_elision_static_inputs_and_overlap_are_bitwise_neutral(cache, 
                 assert np.array_equal(wa, wb)
     for r in runs:
         r.close()
+
+
+@pytest.mark.parametrize("p", [1, 3])
+@pytest.mark.parametrize("gemm", ["fp32", "tf32x3"])
+@pytest.mark.parametrize("quant", [0, 8])
+def test_hoisted_input_aggregation(p, gemm, quant):
+    """static_inputs = 2: layer 1 as (Â_i X_i) W^(0) and ∇W^(0) = (Â_i X_i)ᵀ δ^(1) (no layer-1
+    SpMMs in the epoch) follows the oracle's trajectory within the exact-mode bars (ε = 0);
+    with int8 messages within the 50-epoch loss bar."""
+    require_gpu()
+    d = small_random_graph(900, 5000, (24, 16, 6), seed=67)
+    kw = dict(cache=True, quant_bits=quant, eps0=0.0, adaptive=False, optimizer="sgd", lr=0.5)
+    run = Run(d, p, gemm=gemm, static_inputs=2, **kw)
+    orc = _oracle(d, p, **kw)
+    tl, tw = (1e-5, 1e-4) if quant == 0 else (1e-3, 1e-2)
+    for ep in range(6):
+        g = run.epoch()
+        o = orc.epoch()
+        assert abs(g["loss"] - o["loss"]) <= tl * max(1.0, abs(o["loss"])), (ep, g["loss"], o["loss"])
+        if quant == 0:
+            for wg, wo in zip(run.weights(), orc.W):
+                assert rownorm_err(wg, wo) <= tw
+    run.close()
