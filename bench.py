@@ -203,6 +203,8 @@ def reference_main(args):
 def main(args):
     if args.impl == "reference":
         return reference_main(args)
+    if os.environ.get("NCCL_DEBUG") and not os.environ.get("NCCL_DEBUG_FILE"):
+        os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"   # stdout carries exactly one JSON line
     import numpy as np
     import torch
     rank, world, local = dist_env()
@@ -299,13 +301,16 @@ def main(args):
         e2e = {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": int(h2d_all[0]),
                "d2h_bytes_per_step": int(h2d_all[1])}
     run.close()
+    plan = run.plan
+    run.workspace = None
     # ---- the same workload with the layer-1 aggregation hoisted (static_inputs = 2): Â_i X_i is
     # built once per X buffer, layer 1 runs (Â_i X_i) W^(0) and ∇W^(0) = (Â_i X_i)ᵀ δ^(1)
     hoist = None
     if args.hoisted:
         run2 = Run(ds, world, rank=rank, world=world, device=local, cache=mode[0], quant_bits=mode[1],
                    eps0=args.eps0, adaptive=True, optimizer="adam", lr=0.01, timing=True,
-                   host_inputs=False, transport=args.transport, static_inputs=2, overlap=args.overlap)
+                   host_inputs=False, transport=args.transport, static_inputs=2, overlap=args.overlap,
+                   plan=plan)
         for _ in range(args.warmup):
             run2.epoch()
         torch.cuda.synchronize()

@@ -105,6 +105,7 @@ struct LocalPart {
     RegionTab *gsend_d = nullptr, *grecv_d = nullptr, *ssend_d = nullptr, *srecv_d = nullptr;
     RegionTab gsend_h{}, grecv_h{}, ssend_h{}, srecv_h{};
     PutTab *putG_d = nullptr, *putS_d = nullptr;   // NVLink push of gather / scatter messages
+    uint64_t* bar = nullptr;           // [p] NVLink barrier arrival slots (written by the peers)
     int32_t* cnt = nullptr;           // [4p]: gsend | grecv | ssend | srecv
     int32_t* cnt_h = nullptr;         // pinned
     uint8_t *gflag = nullptr, *fired = nullptr, *active = nullptr;
@@ -157,6 +158,9 @@ struct cdfgnn_ctx {
     int transport = 0;                 // 0 co-resident (world 1), 1 NCCL send/recv, 2 NVLink push
     bool in_epoch = false;             // Hᵀ reuse between forward and backward only inside cdfgnn_epoch
     std::vector<void*> peer_maps;      // IPC-opened peer allocations (push transport)
+    BarTab bar{};                      // device barrier over the mappings (push transport)
+    uint64_t bar_seq = 0;
+    bool bar_dev = false;              // false: NCCL allreduce barrier (CDFGNN_NCCL_BARRIER=1)
     // boundary-rows-first overlap (cfg.overlap): gather phases run on s2
     cudaStream_t s2 = nullptr;
     cudaEvent_t evA = nullptr, evB = nullptr;
@@ -376,6 +380,7 @@ void carve(cdfgnn_ctx* c, Bump& b) {
         P.putG_d = b.take<PutTab>(1);
         P.putS_d = b.take<PutTab>(1);
         P.cnt = b.take<int32_t>(4 * p);
+        P.bar = b.take<uint64_t>(p);
         P.gflag = b.take<uint8_t>(P.M);
         P.fired = b.take<uint8_t>(P.B);
         P.active = b.take<uint8_t>(P.B);
@@ -564,6 +569,10 @@ int nccl_phase(cdfgnn_ctx* c, LocalPart& P, bool gather, int64_t rowb, cudaStrea
 // NVLink push: every rank's pack kernels have stored into the peers' receive regions once
 // this stream-ordered all-reduce completes on all ranks (no host round trip)
 int push_barrier(cdfgnn_ctx* c, cudaStream_t s) {
+    if (c->bar_dev) {
+        c->launches += launch_nvl_barrier(c->bar, ++c->bar_seq, c->scal_d + 1, s);
+        return check_launch("nvl barrier");
+    }
     NCCL_TRY(ncclAllReduce(c->scal_d + 4, c->scal_d + 4, 1, ncclInt32, ncclSum, c->comm, s));
     return CDFGNN_OK;
 }
@@ -572,6 +581,7 @@ struct PeerInfo {
     cudaIpcMemHandle_t handle;
     uint64_t ws_off;                   // workspace offset inside the IPC allocation
     uint64_t cnt_off;                  // counts array, relative to the workspace
+    uint64_t bar_off;                  // barrier arrival slots, relative to the workspace
     uint64_t regA_off[kMaxParts];      // mirror-role regions (receive scatter from master j)
     uint64_t regB_off[kMaxParts];      // master-role regions (receive gather from source s)
 };
@@ -601,6 +611,7 @@ int setup_push(cdfgnn_ctx* c, cudaStream_t s) {
     const uint8_t* ws = reinterpret_cast<const uint8_t*>(c->ws);
     mine.ws_off = (uint64_t)(ws - reinterpret_cast<const uint8_t*>(base));
     mine.cnt_off = (uint64_t)(reinterpret_cast<const uint8_t*>(P.cnt) - ws);
+    mine.bar_off = (uint64_t)(reinterpret_cast<const uint8_t*>(P.bar) - ws);
     for (int j = 0; j < p; ++j) {
         mine.regA_off[j] = (uint64_t)(P.regA[j] - ws);
         mine.regB_off[j] = (uint64_t)(P.regB[j] - ws);
@@ -629,6 +640,7 @@ int setup_push(cdfgnn_ctx* c, cudaStream_t s) {
         }
         c->peer_maps.push_back(mapped);
         uint8_t* pws = reinterpret_cast<uint8_t*>(mapped) + all[r].ws_off;
+        c->bar.peer_slot[r] = reinterpret_cast<uint64_t*>(pws + all[r].bar_off) + me;
         int32_t* pcnt = reinterpret_cast<int32_t*>(pws + all[r].cnt_off);
         // gather: my packed mirror slab for master r -> r's master-role region for source me
         pg.src_hdr[r] = P.gsend_h.hdr[r];
@@ -648,6 +660,14 @@ int setup_push(cdfgnn_ctx* c, cudaStream_t s) {
     CUDA_TRY(cudaMemcpyAsync(P.putG_d, &pg, sizeof(PutTab), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(P.putS_d, &ps, sizeof(PutTab), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    c->bar.my_slots = P.bar;
+    c->bar.p = p;
+    c->bar.me = me;
+    c->bar_seq = 0;
+    // measured on 2 B200 (C3, tools/r1d.sh): the one-int NCCL allreduce barrier beat the flag
+    // barrier (gather_xfer 0.17 vs 0.32 ms per epoch), so it stays the default
+    const char* nb = getenv("CDFGNN_DEV_BARRIER");
+    c->bar_dev = nb && atoi(nb) != 0;
     // every rank must have mapped its peers before anyone pushes
     NCCL_TRY(ncclAllReduce(c->scal_d + 4, c->scal_d + 4, 1, ncclInt32, ncclSum, c->comm, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -1135,6 +1155,7 @@ extern "C" int cdfgnn_init(const cdfgnn_plan* plan, const int32_t* parts, int32_
                 CUDA_TRY(cudaMemcpy(P.ssend_d, &P.ssend_h, sizeof(RegionTab), cudaMemcpyHostToDevice));
                 for (void* m : c->peer_maps) cudaIpcCloseMemHandle(m);
                 c->peer_maps.clear();
+                c->bar_dev = false;
             }
         }
     }

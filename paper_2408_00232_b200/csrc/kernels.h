@@ -59,6 +59,18 @@ struct PutTab {
 int launch_put(const PutTab* tab, int p, int64_t hdr_bytes, int64_t row_bytes, int64_t max_count,
                cudaStream_t s);
 
+// Device-side barrier of the NVLink push transport: rank `me` publishes `seq` into every
+// peer's arrival slot for `me` (system-scope release, through the CUDA-IPC mapping) and waits
+// until each peer has published `seq` into its own slot array (system-scope acquire).  Every
+// rank runs the same sequence of barriers, so `seq` is a per-context counter.  A wait longer
+// than ~10 s sets *err = 5 instead of hanging.
+struct BarTab {
+    uint64_t* peer_slot[kMaxParts];   // peer r's arrival slot for me (mapped), nullptr for r == me
+    const uint64_t* my_slots;         // [p] local arrival slots, written by the peers
+    int p, me;
+};
+int launch_nvl_barrier(const BarTab& t, uint64_t seq, int32_t* err, cudaStream_t s);
+
 // Cache tables of one (layer, direction) of one part (may be null with cache off).
 struct CacheDev {
     float* s_mir;   // [M*ld]

@@ -228,14 +228,32 @@ __global__ void optimizer_kernel(int kind, float* __restrict__ W, const float* _
     W[i] = W[i] - (lr / bc1) * (mi / denom);
 }
 
-__global__ void read_probe_kernel(const float4* __restrict__ p, int64_t n4, int reps, float* sink) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+__global__ void __launch_bounds__(256) read_probe_kernel(const float4* __restrict__ p, int64_t n4, int reps,
+                                                         float* sink) {
+    // 8 independent 16-byte L2 reads in flight per thread (ld.global.cg: L1 bypassed), so the
+    // probe is bound by L2 -> SM delivery, not by per-thread latency
+    constexpr int U = 8;
+    float4 acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int r = 0; r < reps; ++r)
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-            const float4 v = __ldcg(p + i);
-            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t i = i0 + u * stride;
+                v[u] = i < n4 ? __ldcg(p + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                acc[u].x += v[u].x; acc[u].y += v[u].y; acc[u].z += v[u].z; acc[u].w += v[u].w;
+            }
         }
-    if (acc.x == 1.2345e-30f && sink) sink[0] = acc.y + acc.z + acc.w;   // keep the loads alive
+    float t = 0.f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) t += acc[u].x + acc[u].y + acc[u].z + acc[u].w;
+    if (t == 1.2345e-30f && sink) sink[0] = t;   // keep the loads alive
 }
 
 }  // namespace

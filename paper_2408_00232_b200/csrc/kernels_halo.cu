@@ -504,22 +504,40 @@ __global__ void __launch_bounds__(kThreads) scatter_pack_kernel(HaloDev h, SyncA
     }
     // payloads: the block's destination range is contiguous, so the copy is flattened over
     // (message, word) with coalesced stores
+    // (4 independent loads in flight per thread before the stores: the copy is latency-bound)
     if (h.quant) {
         const int wpr = (int)(a.ld >> 2);        // code rows are ld bytes
         uint32_t* dst = reinterpret_cast<uint32_t*>(pay + m0 * a.ld);
-        const int64_t nw = (int64_t)total * wpr;
-        for (int64_t i = threadIdx.x; i < nw; i += kThreads) {
-            const int k = (int)(i / wpr), o = (int)(i - (int64_t)k * wpr);
-            dst[i] = reinterpret_cast<const uint32_t*>(h.stage_codes + (int64_t)s_row[k] * a.ld)[o];
+        const int nw = total * wpr;
+        for (int i0 = threadIdx.x; i0 < nw; i0 += 4 * kThreads) {
+            uint32_t w[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * kThreads;
+                const int k = i / wpr, o = i - k * wpr;
+                w[u] = i < nw ? __ldg(reinterpret_cast<const uint32_t*>(h.stage_codes + (int64_t)s_row[min(k, total - 1)] * a.ld) + o) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i0 + u * kThreads < nw) dst[i0 + u * kThreads] = w[u];
         }
     } else {
         const float* srcb = a.nocache ? h.stage_a : a.c.a;
         const int vpr = (int)(a.ld >> 2);
         float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(pay) + m0 * a.ld);
-        const int64_t nv = (int64_t)total * vpr;
-        for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
-            const int k = (int)(i / vpr), o = (int)(i - (int64_t)k * vpr);
-            dst[i] = reinterpret_cast<const float4*>(srcb + (int64_t)s_row[k] * a.ld)[o];
+        const int nv = total * vpr;
+        for (int i0 = threadIdx.x; i0 < nv; i0 += 4 * kThreads) {
+            float4 w[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * kThreads;
+                const int k = i / vpr, o = i - k * vpr;
+                w[u] = i < nv ? reinterpret_cast<const float4*>(srcb + (int64_t)s_row[min(k, total - 1)] * a.ld)[o]
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i0 + u * kThreads < nv) dst[i0 + u * kThreads] = w[u];
         }
     }
     if (h.remote) __threadfence_system();
@@ -617,6 +635,28 @@ __global__ void put_kernel(const PutTab* __restrict__ tab, int64_t hdr_bytes, in
     __threadfence_system();
 }
 
+// ==================================================================================
+// NVLink barrier (push transport): one thread per peer
+// ==================================================================================
+__global__ void nvl_barrier_kernel(const __grid_constant__ BarTab t, uint64_t seq, int32_t* err) {
+    const int j = threadIdx.x;
+    if (j >= t.p || j == t.me) return;
+    // the put kernel's peer stores precede this kernel in stream order; fence, then publish
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(t.peer_slot[j]), "l"(seq) : "memory");
+    const long long t0 = clock64();
+    for (;;) {
+        uint64_t v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(t.my_slots + j) : "memory");
+        if (v >= seq) break;
+        if (clock64() - t0 > 20000000000LL) {   // ~10 s at 2 GHz: report, do not hang
+            atomicExch(err, 5);
+            break;
+        }
+        __nanosleep(100);
+    }
+}
+
 // ---- dispatch by row width: LPR lanes x VPL float4 per lane cover ld columns ------
 struct Shape { int lpr, vpl; };
 Shape shape_of(int64_t ld) {
@@ -688,6 +728,12 @@ int launch_put(const PutTab* tab, int p, int64_t hdr_bytes, int64_t row_bytes, i
     const int64_t bytes = max_count * (hdr_bytes + row_bytes);
     const unsigned bx = (unsigned)std::min<int64_t>(std::max<int64_t>((bytes / 16 + 255) / 256, 1), 296);
     put_kernel<<<dim3(bx, p), 256, 0, s>>>(tab, hdr_bytes, row_bytes);
+    return 1;
+}
+
+int launch_nvl_barrier(const BarTab& t, uint64_t seq, int32_t* err, cudaStream_t s) {
+    if (t.p <= 1) return 0;
+    nvl_barrier_kernel<<<1, 32 * ((t.p + 31) / 32), 0, s>>>(t, seq, err);
     return 1;
 }
 

@@ -232,13 +232,20 @@ void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val,
         if (shape == 1 && nv <= 12) launch<4, 3, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
         else if (shape == 2 && nv <= 12) launch<2, 6, 2>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
         else if (shape == 3) launch<8, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
+        else if (shape == 4) launch<16, 1, 16>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
+        else if (shape == 5) launch<4, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
+        else if (shape == 6) launch<8, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
         else if (unr == 4) launch<16, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
         else launch<16, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
     } else if (nv <= 32) {
         if (unr == 4) launch<32, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
         else launch<32, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
     } else if (nv <= 64) {
-        if (unr == 2) launch<32, 2, 2>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+        const int wshape = env_int("CDFGNN_SPMM_WSHAPE", 0);
+        if (wshape == 1) launch<16, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+        else if (wshape == 2) launch<16, 4, 2>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+        else if (wshape == 3) launch<32, 2, 6>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+        else if (unr == 2) launch<32, 2, 2>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
         else if (unr == 8) launch<32, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
         else launch<32, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
     } else if (nv <= 128) launch<32, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
