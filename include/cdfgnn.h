@@ -266,6 +266,18 @@ int cdfgnn_epoch_host(cdfgnn_ctx* ctx, const float* const* X_host,
                       const int32_t* const* labels_host, const uint8_t* const* train_mask_host,
                       float* const* W, cdfgnn_epoch_stats* out, void* stream);
 
+/* Pipelined host inputs: runs Alg. 1 once on this step's host inputs and, when X_next /
+ * labels_next / train_mask_next are non-NULL, starts copying the NEXT step's host inputs
+ * into a second context-owned slot on an internal copy stream, overlapping this epoch.  On
+ * the following call those prefetched inputs are used (its X_host/labels/mask arguments are
+ * then ignored and may be NULL).  The *_next host buffers must stay unchanged until the next
+ * call returns.  Errors as cdfgnn_epoch; all three *_next set or all NULL (else EUSAGE). */
+int cdfgnn_epoch_host_next(cdfgnn_ctx* ctx, const float* const* X_host,
+                           const int32_t* const* labels_host, const uint8_t* const* train_mask_host,
+                           const float* const* X_next, const int32_t* const* labels_next,
+                           const uint8_t* const* train_mask_next, float* const* W,
+                           cdfgnn_epoch_stats* out, void* stream);
+
 /* ---- introspection (tests, replay) ---- */
 /* which: 0 mirror snapshot s, 1 mirror view b, 2 master snapshot s, 3 aggregate a,
  *        4 master view b.  Device pointer into the workspace. */

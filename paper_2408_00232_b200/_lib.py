@@ -117,6 +117,8 @@ _sig("cdfgnn_epoch", c_i32, [c_void_p, P(c_void_p), P(c_void_p), P(c_void_p), P(
                              P(EpochStatsC), c_void_p])
 _sig("cdfgnn_epoch_host", c_i32, [c_void_p, P(c_void_p), P(c_void_p), P(c_void_p), P(c_void_p),
                                   P(EpochStatsC), c_void_p])
+_sig("cdfgnn_epoch_host_next", c_i32, [c_void_p, P(c_void_p), P(c_void_p), P(c_void_p), P(c_void_p),
+                                       P(c_void_p), P(c_void_p), P(c_void_p), P(EpochStatsC), c_void_p])
 _sig("cdfgnn_cache_view", c_i32, [c_void_p, c_i32, c_i32, c_i32, c_i32, P(c_void_p), P(c_i64),
                                   P(c_i64)])
 _sig("cdfgnn_sync_flags", c_i32, [c_void_p, c_i32, c_i32, P(c_void_p), P(c_i64)])

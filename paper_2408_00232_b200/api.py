@@ -247,6 +247,25 @@ def epoch_host(ctx: Ctx, X_host: List, labels_host: List, train_host: List, W: L
     return _epoch_dict(st, ctx.cfg.L)
 
 
+def epoch_host_next(ctx: Ctx, X_host: Optional[List], labels_host: Optional[List],
+                    train_host: Optional[List], W: List, X_next: Optional[List] = None,
+                    labels_next: Optional[List] = None, train_next: Optional[List] = None,
+                    stream=None) -> Dict:
+    """cdfgnn_epoch_host_next: this step on host inputs (ignored when the previous call
+    prefetched them) and an overlapped copy of the next step's host inputs (*_next)."""
+    def hp(a):
+        return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+
+    def arr(xs):
+        return L.ptr_array([hp(x) for x in xs]) if xs is not None else None
+    st = L.EpochStatsC()
+    check(_c.cdfgnn_epoch_host_next(ctx.handle, arr(X_host), arr(labels_host), arr(train_host),
+                                    arr(X_next), arr(labels_next), arr(train_next),
+                                    L.ptr_array([_ptr(w) for w in W]), ctypes.byref(st),
+                                    _stream(stream)))
+    return _epoch_dict(st, ctx.cfg.L)
+
+
 def cache_view(ctx: Ctx, local_part: int, l: int, direction: int, which: int):
     """(device pointer, rows, ld) of a cache table (0 s_mir, 1 b_mir, 2 s_mas, 3 a, 4 b_mas)."""
     p = ctypes.c_void_p()

@@ -115,9 +115,12 @@ struct LocalPart {
     CacheDev cache[CDFGNN_MAX_LAYERS][2] = {};
     float* act[CDFGNN_MAX_LAYERS + 1] = {};
     float *T = nullptr, *S = nullptr, *D[2] = {nullptr, nullptr}, *rowloss = nullptr;
-    float* X_stage = nullptr;
+    float* X_stage = nullptr;          // host-input staging, slot 0 ...
     int32_t* lab_stage = nullptr;
     uint8_t* mask_stage = nullptr;
+    float* X_stage1 = nullptr;         // ... and slot 1 (prefetch of the next step's inputs)
+    int32_t* lab_stage1 = nullptr;
+    uint8_t* mask_stage1 = nullptr;
     HaloDev halo{};
 };
 
@@ -165,6 +168,10 @@ struct cdfgnn_ctx {
     cudaStream_t s2 = nullptr;
     cudaEvent_t evA = nullptr, evB = nullptr;
     bool pend[CDFGNN_MAX_LAYERS][2] = {};   // gather of (l, dir) already launched on s2
+    // pipelined host inputs (cdfgnn_epoch_host_next): staging slot prefetched for the next call
+    cudaStream_t cs = nullptr;
+    cudaEvent_t staged[2] = {nullptr, nullptr}, used[2] = {nullptr, nullptr};
+    int prefetched = -1;
 };
 
 namespace {
@@ -414,6 +421,9 @@ void carve(cdfgnn_ctx* c, Bump& b) {
         if (c->cfg.static_inputs == 2) P.ax = b.take<float>(P.n * ld_of(c->cfg.dims[0]));
         P.lab_stage = b.take<int32_t>(P.n);
         P.mask_stage = b.take<uint8_t>(P.n);
+        P.X_stage1 = b.take<float>(P.n * ld_of(c->cfg.dims[0]));
+        P.lab_stage1 = b.take<int32_t>(P.n);
+        P.mask_stage1 = b.take<uint8_t>(P.n);
     }
     c->dW = b.take<float>(c->wtotal);
     c->adam_m = b.take<float>(c->wtotal);
@@ -1188,6 +1198,14 @@ extern "C" int cdfgnn_destroy(cdfgnn_ctx* c) {
     }
     if (c->evA) cudaEventDestroy(c->evA);
     if (c->evB) cudaEventDestroy(c->evB);
+    if (c->cs) {
+        cudaStreamSynchronize(c->cs);
+        cudaStreamDestroy(c->cs);
+    }
+    for (int i = 0; i < 2; ++i) {
+        if (c->staged[i]) cudaEventDestroy(c->staged[i]);
+        if (c->used[i]) cudaEventDestroy(c->used[i]);
+    }
     delete c;
     return CDFGNN_OK;
 }
@@ -1417,6 +1435,79 @@ extern "C" int cdfgnn_epoch(cdfgnn_ctx* c, const float* const* X, const int32_t*
     return rc;
 }
 
+namespace {
+void stage_slot(LocalPart& P, int slot, float** X, int32_t** lab, uint8_t** msk) {
+    *X = slot ? P.X_stage1 : P.X_stage;
+    *lab = slot ? P.lab_stage1 : P.lab_stage;
+    *msk = slot ? P.mask_stage1 : P.mask_stage;
+}
+int copy_inputs(cdfgnn_ctx* c, int slot, const float* const* X_host, const int32_t* const* labels_host,
+                const uint8_t* const* mask_host, cudaStream_t s) {
+    const int64_t ld0 = ld_of(c->cfg.dims[0]);
+    for (int t = 0; t < c->k; ++t) {
+        LocalPart& P = c->parts[t];
+        float* X; int32_t* lab; uint8_t* msk;
+        stage_slot(P, slot, &X, &lab, &msk);
+        CUDA_TRY(cudaMemcpyAsync(X, X_host[t], sizeof(float) * P.n * ld0, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(lab, labels_host[t], sizeof(int32_t) * P.n, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(msk, mask_host[t], P.n, cudaMemcpyHostToDevice, s));
+    }
+    return CDFGNN_OK;
+}
+}  // namespace
+
+extern "C" int cdfgnn_epoch_host_next(cdfgnn_ctx* c, const float* const* X_host,
+                                      const int32_t* const* labels_host,
+                                      const uint8_t* const* train_mask_host,
+                                      const float* const* X_next, const int32_t* const* labels_next,
+                                      const uint8_t* const* train_mask_next, float* const* W,
+                                      cdfgnn_epoch_stats* out, void* stream) {
+    if (!c || !W) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+    if ((X_next != nullptr) != (labels_next != nullptr) || (X_next != nullptr) != (train_mask_next != nullptr))
+        CDF_FAIL(CDFGNN_EUSAGE, "X_next, labels_next and train_mask_next must be all set or all NULL");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!c->cs) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CUDA_TRY(cudaEventCreateWithFlags(&c->staged[i], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&c->used[i], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventRecord(c->used[i], c->cs));
+        }
+    }
+    int cur = c->prefetched;
+    if (cur >= 0) {
+        CUDA_TRY(cudaStreamWaitEvent(s, c->staged[cur], 0));     // this step's inputs, copied under the last step
+    } else {
+        if (!X_host || !labels_host || !train_mask_host) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+        cur = 0;
+        CUDA_TRY(cudaStreamWaitEvent(s, c->used[0], 0));
+        CDF_TRY(copy_inputs(c, 0, X_host, labels_host, train_mask_host, s));
+    }
+    c->prefetched = -1;
+    if (X_next) {
+        // the next step's inputs go to the other slot on the copy stream, overlapping this epoch
+        const int nxt = 1 - cur;
+        CUDA_TRY(cudaStreamWaitEvent(c->cs, c->used[nxt], 0));
+        CDF_TRY(copy_inputs(c, nxt, X_next, labels_next, train_mask_next, c->cs));
+        CUDA_TRY(cudaEventRecord(c->staged[nxt], c->cs));
+        c->prefetched = nxt;
+    }
+    std::vector<const float*> X(c->k);
+    std::vector<const int32_t*> lab(c->k);
+    std::vector<const uint8_t*> msk(c->k);
+    for (int t = 0; t < c->k; ++t) {
+        float* x; int32_t* l; uint8_t* m;
+        stage_slot(c->parts[t], cur, &x, &l, &m);
+        X[t] = x; lab[t] = l; msk[t] = m;
+    }
+    c->in_epoch = true;
+    const int rc = epoch_impl(c, X.data(), lab.data(), msk.data(), W, out, s);
+    c->in_epoch = false;
+    cudaEventRecord(c->used[cur], s);
+    return rc;
+}
+
 extern "C" int cdfgnn_epoch_host(cdfgnn_ctx* c, const float* const* X_host,
                                  const int32_t* const* labels_host,
                                  const uint8_t* const* train_mask_host, float* const* W,
@@ -1424,6 +1515,11 @@ extern "C" int cdfgnn_epoch_host(cdfgnn_ctx* c, const float* const* X_host,
     if (!c || !X_host || !labels_host || !train_mask_host || !W) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
     CUDA_TRY(cudaSetDevice(c->device));
     cudaStream_t s = (cudaStream_t)stream;
+    if (c->prefetched >= 0) {           // a prefetch from cdfgnn_epoch_host_next is discarded
+        CUDA_TRY(cudaStreamWaitEvent(s, c->staged[c->prefetched], 0));
+        c->prefetched = -1;
+    }
+    if (c->cs) CUDA_TRY(cudaStreamWaitEvent(s, c->used[0], 0));
     const int64_t ld0 = ld_of(c->cfg.dims[0]);
     std::vector<const float*> X(c->k);
     std::vector<const int32_t*> lab(c->k);

@@ -81,6 +81,12 @@ class Run:
         return api.epoch_host(self.ctx, self.X_host, self.labels_host, self.masks_host, self.W,
                               stream)
 
+    def epoch_host_next(self, prefetch_next: bool, stream=None) -> Dict:
+        """Host-input epoch; prefetch_next copies the next step's (static) inputs under it."""
+        nx = (self.X_host, self.labels_host, self.masks_host) if prefetch_next else (None, None, None)
+        return api.epoch_host_next(self.ctx, self.X_host, self.labels_host, self.masks_host, self.W,
+                                   *nx, stream)
+
     def weights(self) -> List[np.ndarray]:
         return [w.detach().cpu().numpy() for w in self.W]
 

@@ -184,3 +184,23 @@ def test_hoisted_input_aggregation(p, gemm, quant):
             for wg, wo in zip(run.weights(), orc.W):
                 assert rownorm_err(wg, wo) <= tw
     run.close()
+
+
+def test_pipelined_host_inputs_bitwise():
+    """cdfgnn_epoch_host_next (inputs of step k+1 copied under step k) gives bit-identical
+    losses and weights to cdfgnn_epoch on device inputs."""
+    require_gpu()
+    d = small_random_graph(700, 4000, (20, 16, 5), seed=71)
+    kw = dict(cache=True, quant_bits=8, eps0=0.01, adaptive=True, optimizer="adam", lr=0.01,
+              static_inputs=1)
+    a = Run(d, 2, **kw)
+    b = Run(d, 2, host_inputs=True, **kw)
+    steps = 5
+    for k in range(steps):
+        ga = a.epoch()
+        gb = b.epoch_host_next(prefetch_next=k + 1 < steps)
+        assert ga["loss"] == gb["loss"], (k, ga["loss"], gb["loss"])
+    for wa, wb in zip(a.weights(), b.weights()):
+        assert np.array_equal(wa, wb)
+    a.close()
+    b.close()
