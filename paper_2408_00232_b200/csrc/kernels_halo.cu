@@ -31,14 +31,32 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kScatterTile = 256;
 
 // ---- R15 canonical quantiser (B = 8) ------------------------------------------
-__device__ __forceinline__ uint32_t q8(float d, float lo, float rng) {
-    if (rng == 0.f) return 0u;
-    float t = __fsub_rn(d, lo);
-    t = __fmul_rn(t, 256.f);
-    t = __fdiv_rn(t, rng);
-    t = __fadd_rn(t, 0.5f);
-    float q = floorf(t);
-    return (uint32_t)fminf(q, 255.f);
+// code = min(floor(RN(RN(RN(RN(d − lo)·256) / rng) + 0.5)), 255), 0 when rng = 0.
+// Fast path: y = RN(t·RN(1/rng)) is within 2^-15 of t/rng (t/rng ∈ [0, 256]), so
+// v = RN(y + 0.5) is within 2^-13 of the canonical RN(RN(t/rng) + 0.5); whenever v's
+// fractional part is at least 2^-11 away from an integer both floors agree.  Closer to a
+// boundary the canonical IEEE division decides, so every code is bit-identical to the
+// oracle's fp32 replay (oracle/cache.py) — one reciprocal per row instead of one division
+// per element.
+struct QRow {
+    float lo, rng, rinv;
+};
+__device__ __forceinline__ QRow qrow(float lo, float hi) {
+    QRow q;
+    q.lo = lo;
+    q.rng = __fsub_rn(hi, lo);
+    q.rinv = q.rng == 0.f ? 0.f : __frcp_rn(q.rng);
+    return q;
+}
+__device__ __forceinline__ uint32_t q8(float d, const QRow& q) {
+    if (q.rng == 0.f) return 0u;
+    const float t = __fmul_rn(__fsub_rn(d, q.lo), 256.f);
+    const float v = __fadd_rn(__fmul_rn(t, q.rinv), 0.5f);
+    float fl = floorf(v);
+    const float fr = __fsub_rn(v, fl);
+    if (!(fr > 0.00048828125f && fr < 0.99951171875f))          // within 2^-11 of an integer
+        fl = floorf(__fadd_rn(__fdiv_rn(t, q.rng), 0.5f));
+    return (uint32_t)fminf(fl, 255.f);
 }
 __device__ __forceinline__ float dq8(uint32_t q, float lo, float step) {
     return __fadd_rn(__fmul_rn(step, (float)q), lo);
@@ -185,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 3 : 1) gather_pack_kernel
         const int64_t mrow = s_moff[seg] + ridx[r];
         float* sr = a.nocache ? nullptr : a.c.s_mir + mrow * a.ld;
         if (h.quant) {
-            const float rng = __fsub_rn(hi[r], lo[r]);
+            const QRow qr = qrow(lo[r], hi[r]);
             const float stp = step8(lo[r], hi[r]);
             if (gl == 0) {
                 uint32_t* hp = reinterpret_cast<uint32_t*>(hdr + mm * 12);
@@ -203,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 3 : 1) gather_pack_kernel
                 const float4 s4 = sr ? ld4(sr + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    q[k] = q8(comp(d[r][v], k), lo[r], rng);
+                    q[k] = q8(comp(d[r][v], k), qr);
                     const float sk = (c0 + k < a.F) ? __fadd_rn(comp(s4, k), dq8(q[k], lo[r], stp)) : 0.f;
                     setc(snew, k, sk);
                 }
@@ -398,7 +416,8 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 4 : 1) master_kernel(Halo
     }
     if (act) {
         if (h.quant) {
-            const float rng = __fsub_rn(hi, lo), stp = step8(lo, hi);
+            const QRow qr = qrow(lo, hi);
+            const float stp = step8(lo, hi);
             uint8_t* codes = h.stage_codes + r * a.ld;
             if (gl == 0) { h.stage_lohi[2 * r] = lo; h.stage_lohi[2 * r + 1] = hi; }
 #pragma unroll
@@ -408,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 4 : 1) master_kernel(Halo
                 uint32_t q[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    q[k] = q8(comp(del[v], k), lo, rng);
+                    q[k] = q8(comp(del[v], k), qr);
                     if (c0 + k < a.F) setc(b[v], k, __fadd_rn(comp(b[v], k), dq8(q[k], lo, stp)));
                 }
                 store_codes4(codes, c0, a.F, q);
