@@ -39,7 +39,7 @@ constexpr int kScatterTile = 256;
 // oracle's fp32 replay (oracle/cache.py) — one reciprocal per row instead of one division
 // per element.
 struct QRow {
-    float lo, rng, rinv;
+    float lo, rng, rinv;   // rinv = 0 when rng = 0: the fast path then yields code 0
 };
 __device__ __forceinline__ QRow qrow(float lo, float hi) {
     QRow q;
@@ -48,15 +48,36 @@ __device__ __forceinline__ QRow qrow(float lo, float hi) {
     q.rinv = q.rng == 0.f ? 0.f : __frcp_rn(q.rng);
     return q;
 }
-__device__ __forceinline__ uint32_t q8(float d, const QRow& q) {
-    if (q.rng == 0.f) return 0u;
+// fast-path floor of RN(RN(t/rng) + 0.5); *slow is set when the canonical division must decide
+__device__ __forceinline__ float q8_fast(float d, const QRow& q, bool* slow) {
     const float t = __fmul_rn(__fsub_rn(d, q.lo), 256.f);
     const float v = __fadd_rn(__fmul_rn(t, q.rinv), 0.5f);
-    float fl = floorf(v);
+    const float fl = floorf(v);
     const float fr = __fsub_rn(v, fl);
-    if (!(fr > 0.00048828125f && fr < 0.99951171875f))          // within 2^-11 of an integer
-        fl = floorf(__fadd_rn(__fdiv_rn(t, q.rng), 0.5f));
-    return (uint32_t)fminf(fl, 255.f);
+    *slow = !(fr > 0.00048828125f && fr < 0.99951171875f);      // within 2^-11 of an integer
+    return fl;
+}
+__device__ __noinline__ float q8_slow(float d, const QRow& q) {
+    if (q.rng == 0.f) return 0.f;
+    const float t = __fmul_rn(__fsub_rn(d, q.lo), 256.f);
+    return floorf(__fadd_rn(__fdiv_rn(t, q.rng), 0.5f));
+}
+// 4 codes of one float4 chunk; the (rare) canonical division runs only for flagged elements
+__device__ __forceinline__ void q8x4(const float (&d)[4], const QRow& q, uint32_t (&c)[4]) {
+    float fl[4];
+    bool sl[4], any = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        fl[k] = q8_fast(d[k], q, &sl[k]);
+        any |= sl[k];
+    }
+    if (any) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (sl[k]) fl[k] = q8_slow(d[k], q);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = (uint32_t)fminf(fl[k], 255.f);
 }
 __device__ __forceinline__ float dq8(uint32_t q, float lo, float step) {
     return __fadd_rn(__fmul_rn(step, (float)q), lo);
@@ -114,7 +135,7 @@ __device__ __forceinline__ int find_seg(const int64_t* off, int p, int64_t idx) 
 // message buffer comes from the decoupled look-back, so the buffer keeps halo-list order.
 // ==================================================================================
 template <int LPR, int VPL, int RPW>
-__global__ void __launch_bounds__(kThreads, VPL <= 2 ? 3 : 1) gather_pack_kernel(HaloDev h, SyncArgs a) {
+__global__ void __launch_bounds__(kThreads, VPL <= 2 ? 2 : 1) gather_pack_kernel(HaloDev h, SyncArgs a) {
     constexpr int GPW = 32 / LPR;
     constexpr int TR = kWarps * GPW * RPW;
     __shared__ int s_wcnt[kWarps];
@@ -135,7 +156,9 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 3 : 1) gather_pack_kernel
     const int ltile = tile - tbase;
     const int64_t seg_len = s_moff[seg + 1] - s_moff[seg];
     const int g = lane / LPR, gl = lane % LPR;
-    float4 d[RPW][VPL];
+    // all RPW rows' z and s chunks are loaded before any is used, so a warp keeps
+    // RPW x VPL x 2 sixteen-byte loads in flight (they stay in registers for the pack below)
+    float4 xs[RPW][VPL], ss[RPW][VPL];
     float lo[RPW], hi[RPW];
     bool flag[RPW];
     unsigned bal[RPW];
@@ -147,36 +170,44 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 3 : 1) gather_pack_kernel
         const int64_t mrow = s_moff[seg] + (valid ? ridx[r] : 0);     // mirror index
         const float* xr = a.X + (h.B + mrow) * a.ld;
         const float* sr = a.nocache ? nullptr : a.c.s_mir + mrow * a.ld;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+            const int c0 = (gl + v * LPR) * 4;
+            xs[r][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            ss[r][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (valid && c0 < a.ld) {
+                xs[r][v] = __ldcs(reinterpret_cast<const float4*>(xr + c0));   // read once: evict-first
+                if (sr) ss[r][v] = __ldcs(reinterpret_cast<const float4*>(sr + c0));
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+        const bool valid = ridx[r] < seg_len;
         float maxd = 0.f, maxs = 0.f;
         lo[r] = INFINITY;
         hi[r] = -INFINITY;
 #pragma unroll
         for (int v = 0; v < VPL; ++v) {
             const int c0 = (gl + v * LPR) * 4;
-            float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f), s4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (valid && c0 < a.ld) {
-                x4 = __ldcs(reinterpret_cast<const float4*>(xr + c0));   // read once: evict-first
-                if (sr) s4 = ld4(sr + c0);
-            }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const float dk = __fsub_rn(comp(x4, k), comp(s4, k));
-                setc(d[r][v], k, dk);
+                const float dk = __fsub_rn(comp(xs[r][v], k), comp(ss[r][v], k));
                 if (c0 + k < a.F) {
-                    maxd = fmaxf(maxd, fabsf(dk));
-                    maxs = fmaxf(maxs, fabsf(comp(s4, k)));
+                    maxs = fmaxf(maxs, fabsf(comp(ss[r][v], k)));
                     lo[r] = fminf(lo[r], dk);
                     hi[r] = fmaxf(hi[r], dk);
                 }
             }
         }
-        maxd = gmax<LPR>(maxd);
         maxs = gmax<LPR>(maxs);
         lo[r] = gmin<LPR>(lo[r]);
         hi[r] = gmax<LPR>(hi[r]);
+        // ‖d‖∞ = max(|min d|, |max d|): exact, no separate reduction
+        maxd = (ridx[r] < seg_len) ? fmaxf(fabsf(lo[r]), fabsf(hi[r])) : 0.f;
         flag[r] = valid && (a.nocache || maxd > __fmul_rn(a.eps, maxs));
         bal[r] = __ballot_sync(0xffffffffu, flag[r] && gl == 0);
-        if (valid && gl == 0) h.gflag[mrow] = flag[r] ? 1 : 0;
+        if (valid && gl == 0) h.gflag[s_moff[seg] + ridx[r]] = flag[r] ? 1 : 0;
     }
     int wcnt = 0;
 #pragma unroll
@@ -218,10 +249,13 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 3 : 1) gather_pack_kernel
                 if (c0 >= a.F) continue;
                 uint32_t q[4];
                 float4 snew = make_float4(0.f, 0.f, 0.f, 0.f);
-                const float4 s4 = sr ? ld4(sr + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 s4 = ss[r][v];
+                float dd[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) dd[k] = __fsub_rn(comp(xs[r][v], k), comp(s4, k));
+                q8x4(dd, qr, q);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    q[k] = q8(comp(d[r][v], k), qr);
                     const float sk = (c0 + k < a.F) ? __fadd_rn(comp(s4, k), dq8(q[k], lo[r], stp)) : 0.f;
                     setc(snew, k, sk);
                 }
@@ -231,13 +265,15 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 3 : 1) gather_pack_kernel
         } else {
             if (gl == 0) reinterpret_cast<uint32_t*>(hdr)[mm] = (uint32_t)ridx[r];
             float* prow = reinterpret_cast<float*>(pay) + mm * a.ld;
-            const float* xr = a.X + (h.B + mrow) * a.ld;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
                 if (c0 >= a.ld) continue;
-                st4(prow + c0, d[r][v]);
-                if (sr) st4(sr + c0, ld4(xr + c0));   // Alg. 2 L6: s ← z
+                float4 dv;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) setc(dv, k, __fsub_rn(comp(xs[r][v], k), comp(ss[r][v], k)));
+                st4(prow + c0, dv);
+                if (sr) st4(sr + c0, xs[r][v]);   // Alg. 2 L6: s ← z
             }
         }
     }
@@ -425,11 +461,11 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 4 : 1) master_kernel(Halo
                 const int c0 = (gl + v * LPR) * 4;
                 if (c0 >= a.F) continue;
                 uint32_t q[4];
+                const float dd[4] = {del[v].x, del[v].y, del[v].z, del[v].w};
+                q8x4(dd, qr, q);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    q[k] = q8(comp(del[v], k), qr);
+                for (int k = 0; k < 4; ++k)
                     if (c0 + k < a.F) setc(b[v], k, __fadd_rn(comp(b[v], k), dq8(q[k], lo, stp)));
-                }
                 store_codes4(codes, c0, a.F, q);
             }
         } else {
