@@ -346,8 +346,8 @@ int prepare(cdfgnn_ctx* c, const cdfgnn_plan* plan, const int32_t* parts, int32_
         }
         // wide rows: LPT over whole rows (chunks cost L2 bandwidth there, profiles/r1);
         // narrow rows: hub rows split into chunks (their latency chains dominated)
-        build_spmm_items(P, P.sp[0], spmm_chunk(true), spmm_default_phases(), spmm_phase_min_degree());
-        build_spmm_items(P, P.sp[1], spmm_chunk(false), spmm_default_phases(), spmm_phase_min_degree());
+        build_spmm_items(P, P.sp[0], spmm_chunk(true, P.nnz), spmm_default_phases(), spmm_phase_min_degree());
+        build_spmm_items(P, P.sp[1], spmm_chunk(false, P.nnz), spmm_default_phases(), spmm_phase_min_degree());
         P.sp[0].pstride = c->ldmax;
         P.sp[1].pstride = std::min<int64_t>(c->ldmax, 64);
     }

@@ -464,7 +464,7 @@ __global__ void splitk_sum_kernel(int64_t M, int64_t N, int64_t ldw, int splits,
 __global__ void transpose_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
                                  float* __restrict__ dst, int64_t ldd) {
     __shared__ float tile[32][33];
-    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;   // rows on grid.x
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
         const int64_t r = r0 + i, c = c0 + threadIdx.x;
         tile[i][threadIdx.x] = (r < rows && c < cols) ? src[r * lds + c] : 0.f;
@@ -480,7 +480,7 @@ __global__ void transpose_kernel(const float* __restrict__ src, int64_t rows, in
 __global__ void relu_transpose_kernel(const float* __restrict__ Z, int64_t rows, int64_t cols, int64_t ldz,
                                       float* __restrict__ H, float* __restrict__ Ht, int64_t ldt) {
     __shared__ float tile[32][33];
-    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;   // rows on grid.x
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
         const int64_t r = r0 + i, c = c0 + threadIdx.x;
         float v = 0.f;
@@ -611,7 +611,7 @@ int pick_bn(int64_t N, bool split3) {
 int launch_transpose(const float* src, int64_t rows, int64_t cols, int64_t lds, float* dst, int64_t ldd,
                      cudaStream_t s) {
     if (rows <= 0 || cols <= 0) return 0;
-    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+    dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32));
     transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, lds, dst, ldd);
     return 1;
 }
@@ -619,7 +619,7 @@ int launch_transpose(const float* src, int64_t rows, int64_t cols, int64_t lds, 
 int launch_relu_transpose(const float* Z, int64_t rows, int64_t cols, int64_t ldz, float* H, float* Ht,
                           int64_t ldt, cudaStream_t s) {
     if (rows <= 0) return 0;
-    dim3 grid((unsigned)((ldz + 31) / 32), (unsigned)((rows + 31) / 32));
+    dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((ldz + 31) / 32));
     relu_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(Z, rows, cols, ldz, H, Ht, ldt);
     return 1;
 }

@@ -116,7 +116,7 @@ struct SpmmItems {
     float* partial;             // [slots x ld] segment partials
     int32_t* counter;           // [slots] segments finished per split row (at its first slot; zero at rest)
 };
-int spmm_chunk(bool wide);
+int spmm_chunk(bool wide, int64_t nnz);
 int spmm_default_phases();
 int spmm_phase_min_degree();
 void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val, int64_t n_items,

@@ -16,6 +16,7 @@
 // run-to-run deterministic regardless of which warp finishes last.  Unsplit rows are
 // visited longest-first (LPT).
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -206,9 +207,16 @@ int env_int(const char* name, int dflt) {
 
 }  // namespace
 
-// chunk length for the wide (ld > 64) and narrow row classes; 0 = no chunking
-int spmm_chunk(bool wide) {
-    return wide ? env_int("CDFGNN_SPMM_CHUNK_WIDE", 0) : env_int("CDFGNN_SPMM_CHUNK", 2048);
+// chunk length for the wide (ld > 64) and narrow row classes; 0 = no chunking.  Narrow rows:
+// about the average work of one resident row group (148 SMs x 64 warps x 4 groups of the
+// 8-lane shape), rounded to a power of two in [512, 4096] — C3 44-wide: 4096 at p=1
+// (1.46 ms vs 2.08 unchunked), 1024 at p=4 (0.40 vs 0.47 ms at 2048; tools/spmm_bench.py)
+int spmm_chunk(bool wide, int64_t nnz) {
+    if (wide) return env_int("CDFGNN_SPMM_CHUNK_WIDE", 0);
+    const double per_group = (double)std::max<int64_t>(nnz, 1) / (148.0 * 64.0 * 4.0);
+    int c = 1 << (int)std::lround(std::log2(std::max(per_group, 1.0)));
+    c = std::min(std::max(c, 512), 4096);
+    return env_int("CDFGNN_SPMM_CHUNK", c);
 }
 int spmm_default_phases() { return env_int("CDFGNN_SPMM_PHASES", 1); }
 int spmm_phase_min_degree() { return env_int("CDFGNN_SPMM_PHASE_MIN", 64); }
