@@ -9,8 +9,8 @@ timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/final_bench.json 
 timeout 300 $B > gpurun_out/fplain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final_launches_C3_p1.csv $B > gpurun_out/fncu_l.log 2>&1
 timeout 300 $B > gpurun_out/fplain2.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"spmm_kernel<32" -s 2 -c 1 -o gpurun_out/final_spmm_wide $B > gpurun_out/fncu_sw.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"spmm_kernel<8" -s 2 -c 1 -o gpurun_out/final_spmm_narrow $B > gpurun_out/fncu_sn.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"spmm_kernel<.int.32," -s 2 -c 1 -o gpurun_out/final_spmm_wide $B > gpurun_out/fncu_sw.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"spmm_kernel<.int.8," -s 2 -c 1 -o gpurun_out/final_spmm_narrow $B > gpurun_out/fncu_sn.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tf32 -s 3 -c 1 -o gpurun_out/final_gemm $B > gpurun_out/fncu_g.log 2>&1
 timeout 300 $H2 > gpurun_out/fplain3.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none -k regex:"gather_pack|master_kernel|mirror_apply|scatter_pack|put_kernel" -s 30 -c 20 -o gpurun_out/final_halo_C3_p2 $H2 > gpurun_out/fncu_h.log 2>&1
