@@ -18,7 +18,6 @@
 // round-to-nearest intrinsics (no FMA contraction) in the canonical order of
 // reading R15, so masks and codes are bit-identical to oracle/cache.py's fp32 replay.
 #include <cuda/atomic>
-#include <cuda_pipeline.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -512,54 +511,6 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 4 : 1) master_kernel(Halo
     master_row<LPR, VPL>(h, a, rt, lane, g, gl, r, valid, xr, smr, bmr, acc, x, s4v, b);
 }
 
-// Persistent variant for 32-lane rows with the cache on: each warp walks rows r, r + W, ...
-// and stages the next row's aggregate / own value / snapshot / scatter base in shared memory
-// with cp.async while it processes the current one, so a row's 4·ld·4 bytes of loads are in
-// flight without holding registers (2 rows in flight per warp, 24 warps per SM).
-template <int VPL>
-__global__ void __launch_bounds__(kThreads, 3) master_cp_kernel(HaloDev h, SyncArgs a,
-                                                                const __grid_constant__ RegionTab rt) {
-    extern __shared__ float4 msm[];     // [warp][stage 2][array 4][VPL][32 lanes]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float4* ws = msm + (size_t)warp * (2 * 4 * VPL * 32);
-    const int64_t W = (int64_t)gridDim.x * kWarps;
-    int64_t row = (int64_t)blockIdx.x * kWarps + warp;
-    const float* src[4] = {a.c.a, a.X, a.c.s_mas, a.c.b_mas};
-    auto issue = [&](int64_t rr, int st) {
-        if (rr < h.B) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int v = 0; v < VPL; ++v) {
-                    const int c0 = (lane + v * 32) * 4;
-                    if (c0 < a.ld)
-                        __pipeline_memcpy_async(&ws[((st * 4 + q) * VPL + v) * 32 + lane], src[q] + rr * a.ld + c0, 16);
-                }
-        }
-        __pipeline_commit();
-    };
-    issue(row, 0);
-    for (int it = 0; row < h.B; ++it, row += W) {
-        const int st = it & 1;
-        issue(row + W, st ^ 1);
-        __pipeline_wait_prior(1);       // this row's group has landed
-        float4 acc[VPL], x[VPL], s4v[VPL], b[VPL];
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-            const int c0 = (lane + v * 32) * 4;
-            const bool in = c0 < a.ld;
-            const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            acc[v] = in ? ws[((st * 4 + 0) * VPL + v) * 32 + lane] : z4;
-            x[v] = in ? ws[((st * 4 + 1) * VPL + v) * 32 + lane] : z4;
-            s4v[v] = in ? ws[((st * 4 + 2) * VPL + v) * 32 + lane] : z4;
-            b[v] = in ? ws[((st * 4 + 3) * VPL + v) * 32 + lane] : z4;
-        }
-        master_row<32, VPL>(h, a, rt, lane, 0, lane, row, true, a.X + row * a.ld, a.c.s_mas + row * a.ld,
-                            a.c.b_mas + row * a.ld, acc, x, s4v, b);
-    }
-    __pipeline_wait_prior(0);
-}
-
 // ==================================================================================
 // scatter_pack: one tile = 256 halo-list entries of one mirror peer
 // ==================================================================================
@@ -874,19 +825,6 @@ int launch_map(const HaloDev& h, const RegionTab& rt, int mirror_side, int64_t m
 
 int launch_master(const HaloDev& h, const SyncArgs& a, const RegionTab& rt, cudaStream_t s) {
     if (h.B <= 0) return 0;
-    const Shape sh0 = shape_of(a.ld);
-    static const int use_cp = [] { const char* e = getenv("CDFGNN_MASTER_CP"); return e ? atoi(e) : 1; }();
-    if (use_cp && !a.nocache && sh0.lpr == 32 && sh0.vpl == 2) {
-        const size_t smem = (size_t)kWarps * 2 * 4 * 2 * 32 * sizeof(float4);   // 64 KB
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(master_cp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
-        const int64_t blocks = std::min<int64_t>((h.B + kWarps - 1) / kWarps, 148 * 3);
-        master_cp_kernel<2><<<(unsigned)blocks, kThreads, smem, s>>>(h, a, rt);
-        return 1;
-    }
     auto grid = [&](int lpr) {
         const int64_t rows_per_block = kWarps * (32 / lpr);
         return (unsigned)((h.B + rows_per_block - 1) / rows_per_block);
