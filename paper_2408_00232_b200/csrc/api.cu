@@ -119,6 +119,7 @@ struct LocalPart {
     int32_t* lab_stage = nullptr;
     uint8_t* mask_stage = nullptr;
     float* X_stage1 = nullptr;         // ... and slot 1 (prefetch of the next step's inputs)
+    float* xpack = nullptr;            // world > 1: master rows of X packed per mirror peer
     int32_t* lab_stage1 = nullptr;
     uint8_t* mask_stage1 = nullptr;
     HaloDev halo{};
@@ -172,6 +173,9 @@ struct cdfgnn_ctx {
     cudaStream_t cs = nullptr;
     cudaEvent_t staged[2] = {nullptr, nullptr}, used[2] = {nullptr, nullptr};
     int prefetched = -1;
+    // world > 1: input rows of mirrors are filled from their masters over NCCL (own communicator,
+    // issued only on the copy stream cs), so each vertex's features cross PCIe once
+    ncclComm_t comm_in = nullptr;
 };
 
 namespace {
@@ -422,6 +426,7 @@ void carve(cdfgnn_ctx* c, Bump& b) {
         P.lab_stage = b.take<int32_t>(P.n);
         P.mask_stage = b.take<uint8_t>(P.n);
         P.X_stage1 = b.take<float>(P.n * ld_of(c->cfg.dims[0]));
+        if (c->k == 1 && p > 1) P.xpack = b.take<float>(P.hoff[p] * ld_of(c->cfg.dims[0]));   // one part per rank
         P.lab_stage1 = b.take<int32_t>(P.n);
         P.mask_stage1 = b.take<uint8_t>(P.n);
     }
@@ -1146,6 +1151,20 @@ extern "C" int cdfgnn_init(const cdfgnn_plan* plan, const int32_t* parts, int32_
         ncclUniqueId id;
         std::memcpy(&id, nccl_uid, sizeof(id));
         NCCL_TRY(ncclCommInitRank(&c->comm, world, id, rank));
+        NCCL_TRY(ncclCommSplit(c->comm, 0, rank, &c->comm_in, nullptr));
+        {
+            // establish the input-distribution peer connections now (NCCL connects p2p lazily,
+            // which would otherwise land inside the first pipelined epochs)
+            float* tmp = reinterpret_cast<float*>(c->splitk);
+            NCCL_TRY(ncclGroupStart());
+            for (int q = 0; q < world; ++q) {
+                if (q == rank) continue;
+                NCCL_TRY(ncclSend(tmp, 1, ncclFloat32, q, c->comm_in, s));
+                NCCL_TRY(ncclRecv(tmp + 1 + q, 1, ncclFloat32, q, c->comm_in, s));
+            }
+            NCCL_TRY(ncclGroupEnd());
+            CUDA_TRY(cudaStreamSynchronize(s));
+        }
         c->transport = 1;
         if (cfg->transport == 0) {
             // all ranks must agree: push only if every rank mapped its peers
@@ -1186,6 +1205,7 @@ extern "C" int cdfgnn_destroy(cdfgnn_ctx* c) {
     if (!c) return CDFGNN_OK;
     if (!c->peer_maps.empty()) cudaDeviceSynchronize();
     for (void* m : c->peer_maps) cudaIpcCloseMemHandle(m);
+    if (c->comm_in) ncclCommDestroy(c->comm_in);
     if (c->comm) ncclCommDestroy(c->comm);
     for (LocalPart& P : c->parts)
         if (P.cnt_h) cudaFreeHost(P.cnt_h);
@@ -1448,9 +1468,35 @@ int copy_inputs(cdfgnn_ctx* c, int slot, const float* const* X_host, const int32
         LocalPart& P = c->parts[t];
         float* X; int32_t* lab; uint8_t* msk;
         stage_slot(P, slot, &X, &lab, &msk);
-        CUDA_TRY(cudaMemcpyAsync(X, X_host[t], sizeof(float) * P.n * ld0, cudaMemcpyHostToDevice, s));
+        if (c->comm_in) {
+            // owned rows only (boundary masters [0, B), interior [B + M, n)); the M mirror rows
+            // are replicas of other parts' masters and arrive from them below
+            CUDA_TRY(cudaMemcpyAsync(X, X_host[t], sizeof(float) * P.B * ld0, cudaMemcpyHostToDevice, s));
+            const int64_t i0 = P.B + P.M;
+            CUDA_TRY(cudaMemcpyAsync(X + i0 * ld0, X_host[t] + i0 * ld0, sizeof(float) * (P.n - i0) * ld0,
+                                     cudaMemcpyHostToDevice, s));
+        } else {
+            CUDA_TRY(cudaMemcpyAsync(X, X_host[t], sizeof(float) * P.n * ld0, cudaMemcpyHostToDevice, s));
+        }
         CUDA_TRY(cudaMemcpyAsync(lab, labels_host[t], sizeof(int32_t) * P.n, cudaMemcpyHostToDevice, s));
         CUDA_TRY(cudaMemcpyAsync(msk, mask_host[t], P.n, cudaMemcpyHostToDevice, s));
+        if (c->comm_in) {
+            // masters' rows for every mirror peer q (halo list order = q's mirror slab order, R21)
+            const int p = c->p, me = P.part;
+            c->launches += launch_gather_rows(X, ld0, P.halo_local, P.hoff[p], P.xpack, s);
+            CDF_TRY(check_launch("gather_rows"));
+            NCCL_TRY(ncclGroupStart());
+            for (int q = 0; q < p; ++q) {
+                if (q == me) continue;
+                if (P.capB[q] > 0)
+                    NCCL_TRY(ncclSend(P.xpack + P.hoff[q] * ld0, (size_t)(P.capB[q] * ld0), ncclFloat32, q,
+                                      c->comm_in, s));
+                if (P.capA[q] > 0)
+                    NCCL_TRY(ncclRecv(X + (P.B + P.moff[q]) * ld0, (size_t)(P.capA[q] * ld0), ncclFloat32, q,
+                                      c->comm_in, s));
+            }
+            NCCL_TRY(ncclGroupEnd());
+        }
     }
     return CDFGNN_OK;
 }
@@ -1481,8 +1527,13 @@ extern "C" int cdfgnn_epoch_host_next(cdfgnn_ctx* c, const float* const* X_host,
     } else {
         if (!X_host || !labels_host || !train_mask_host) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
         cur = 0;
-        CUDA_TRY(cudaStreamWaitEvent(s, c->used[0], 0));
-        CDF_TRY(copy_inputs(c, 0, X_host, labels_host, train_mask_host, s));
+        // on the copy stream (the only stream that issues comm_in operations), then joined
+        CUDA_TRY(cudaEventRecord(c->staged[1], s));
+        CUDA_TRY(cudaStreamWaitEvent(c->cs, c->staged[1], 0));
+        CUDA_TRY(cudaStreamWaitEvent(c->cs, c->used[0], 0));
+        CDF_TRY(copy_inputs(c, 0, X_host, labels_host, train_mask_host, c->cs));
+        CUDA_TRY(cudaEventRecord(c->staged[0], c->cs));
+        CUDA_TRY(cudaStreamWaitEvent(s, c->staged[0], 0));
     }
     c->prefetched = -1;
     if (X_next) {

@@ -256,7 +256,24 @@ __global__ void __launch_bounds__(256) read_probe_kernel(const float4* __restric
     if (t == 1.2345e-30f && sink) sink[0] = t;   // keep the loads alive
 }
 
+// out[k] = X[idx[k]]: flattened over (row, float4), grid-stride
+__global__ void gather_rows_kernel(const float* __restrict__ X, int64_t ld, const int32_t* __restrict__ idx,
+                                   int64_t count, float* __restrict__ out) {
+    const int64_t v4 = ld / 4, total = count * v4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = i / v4, c = i - k * v4;
+        reinterpret_cast<float4*>(out)[i] = reinterpret_cast<const float4*>(X + (int64_t)__ldg(idx + k) * ld)[c];
+    }
+}
+
 }  // namespace
+
+int launch_gather_rows(const float* X, int64_t ld, const int32_t* idx, int64_t count, float* out, cudaStream_t s) {
+    if (count <= 0) return 0;
+    const int64_t total = count * (ld / 4);
+    gather_rows_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(X, ld, idx, count, out);
+    return 1;
+}
 
 void launch_read_probe(const float4* p, int64_t n4, int reps, float* sink, cudaStream_t s) {
     read_probe_kernel<<<148 * 8, 256, 0, s>>>(p, n4, reps, sink);

@@ -32,6 +32,21 @@ def test_two_gpus_match_one_gpu(mode, transport, overlap):
     assert json.loads(lines[-1])["mgpu_check"] == "PASS"
 
 
+def test_two_gpus_pipelined_host_inputs_bitwise():
+    """cdfgnn_epoch_host_next at N = 2: owned rows over PCIe, mirror rows from their masters over
+    NCCL, next step prefetched — losses and W bit-identical to device-resident inputs."""
+    torch = require_gpu()
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29519",
+           os.path.join(ROOT, "tools", "mgpu_check.py"), "--mode", "cache_int8", "--epochs", "4", "--host-next"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert json.loads(lines[-1])["mgpu_check"] == "PASS"
+
+
 def test_two_gpus_full_size_C3_match_unpartitioned():
     """The bench workload at full size on 2 GPUs (NVLink push), exact mode (ε = 0, fp32
     messages): per-epoch loss and W equal the unpartitioned p = 1 model's (P-C1) and the

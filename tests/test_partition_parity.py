@@ -25,6 +25,8 @@ def test_library_exports_every_header_symbol():
     exported = set(re.findall(r"\bT (cdfgnn_[a-z0-9_]+)", out))
     assert declared, "no declarations parsed"
     assert declared <= exported, f"missing: {sorted(declared - exported)}"
+    undefined = subprocess.run(["nm", "-D", "--undefined-only", lib], capture_output=True, text=True).stdout
+    assert "cdfgnn" not in undefined, "library references cdfgnn symbols it does not define"
 
 
 def _compare(d, p, hosts=1, order=1, oorder="degsum", gamma=(1, 10), self_loops=False, seed=0):

@@ -22,6 +22,9 @@ def main():
     ap.add_argument("--mode", default="cache_int8")
     ap.add_argument("--transport", default="push")
     ap.add_argument("--overlap", type=int, default=0)
+    ap.add_argument("--host-next", action="store_true",
+                    help="also run the pipelined host-input path (owned rows over PCIe, mirror rows "
+                         "over NCCL) and require bit-identical losses and W")
     ap.add_argument("--vs-p1", action="store_true",
                     help="rank 0 also runs the unpartitioned p = 1 model (exact mode: P-C1 at full size)")
     a = ap.parse_args()
@@ -54,11 +57,23 @@ def main():
     run = Run(ds, world, rank=rank, world=world, device=local, transport=a.transport,
               overlap=bool(a.overlap), **kw)
     ref = Run(ds, world, device=local, plan=run.plan, **kw) if rank == 0 else None
+    hrun = (Run(ds, world, rank=rank, world=world, device=local, transport=a.transport, plan=run.plan,
+                host_inputs=True, **kw) if a.host_next else None)
     one = Run(ds, 1, device=local, **kw) if (rank == 0 and a.vs_p1) else None
     ok = True
     rows = []
     for ep in range(a.epochs):
         g = run.epoch()
+        if hrun is not None:
+            gh = hrun.epoch_host_next(prefetch_next=ep + 1 < a.epochs)
+            hsame = gh["loss"] == g["loss"] and all(torch.equal(x, y) for x, y in zip(hrun.W, run.W))
+            hs = torch.tensor([0 if hsame else 1], dtype=torch.int32, device="cuda")
+            dist.all_reduce(hs)
+            if hs.item() != 0:
+                ok = False
+                if rank == 0:
+                    print(json.dumps({"epoch": ep, "host_next_mismatch": True, "loss": g["loss"],
+                                      "loss_host": gh["loss"]}), flush=True)
         # bit-identical replicated W across ranks
         flat = torch.cat([w.flatten() for w in run.W])
         allw = [torch.empty_like(flat) for _ in range(world)]
@@ -94,6 +109,8 @@ def main():
         print(json.dumps({"mgpu_check": "PASS" if ok else "FAIL", "world": world, "mode": a.mode}),
               flush=True)
     run.close()
+    if hrun:
+        hrun.close()
     if ref:
         ref.close()
     if one:
