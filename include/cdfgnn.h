@@ -271,7 +271,11 @@ int cdfgnn_epoch_host(cdfgnn_ctx* ctx, const float* const* X_host,
  * into a second context-owned slot on an internal copy stream, overlapping this epoch.  On
  * the following call those prefetched inputs are used (its X_host/labels/mask arguments are
  * then ignored and may be NULL).  The *_next host buffers must stay unchanged until the next
- * call returns.  Errors as cdfgnn_epoch; all three *_next set or all NULL (else EUSAGE). */
+ * call returns.  With one part per rank (world > 1) only the part's owned rows of X_host are
+ * read — boundary masters [0, B) and interior rows [B + M, n); the M mirror rows are filled
+ * from their masters' rows over NCCL (each vertex's features cross PCIe once), so mirror rows
+ * of X_host need not be initialised.  Errors as cdfgnn_epoch; all three *_next set or all
+ * NULL (else EUSAGE). */
 int cdfgnn_epoch_host_next(cdfgnn_ctx* ctx, const float* const* X_host,
                            const int32_t* const* labels_host, const uint8_t* const* train_mask_host,
                            const float* const* X_next, const int32_t* const* labels_next,
