@@ -497,6 +497,56 @@ __global__ void relu_transpose_kernel(const float* __restrict__ Z, int64_t rows,
     }
 }
 
+// 64 x 64 tiles, 16-byte loads and stores, 4 in flight per thread each way (the 32 x 32 scalar
+// kernels above reached ~60% of HBM on the C4 wide transposes).  RELU: also writes
+// H = max(Z, 0) row-major over all lds columns.  Needs lds, ldd % 4 == 0 and 16-B aligned bases.
+template <bool RELU>
+__global__ void __launch_bounds__(256) transpose64_kernel(const float* src, int64_t rows,   // src may alias H
+                                                          int64_t cols, int64_t lds, float* H,
+                                                          float* __restrict__ dst, int64_t ldd) {
+    __shared__ float tile[64][65];
+    const int64_t r0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 64;
+    const int t = threadIdx.x;
+    const int cq = t & 15, rr = t >> 4;
+    float4 v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t r = r0 + rr + 16 * i, c = c0 + 4 * cq;
+        v[i] = (r < rows && c < lds) ? *reinterpret_cast<const float4*>(src + r * lds + c)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (RELU) {
+            v[i].x = fmaxf(v[i].x, 0.f); v[i].y = fmaxf(v[i].y, 0.f);
+            v[i].z = fmaxf(v[i].z, 0.f); v[i].w = fmaxf(v[i].w, 0.f);
+            const int64_t r = r0 + rr + 16 * i, c = c0 + 4 * cq;
+            if (r < rows && c < lds) *reinterpret_cast<float4*>(H + r * lds + c) = v[i];
+        }
+        float* tr = &tile[rr + 16 * i][4 * cq];
+        tr[0] = v[i].x; tr[1] = v[i].y; tr[2] = v[i].z; tr[3] = v[i].w;
+    }
+    __syncthreads();
+    const int rq = t & 15;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int oc = (t >> 4) + 16 * j;
+        const int64_t c = c0 + oc, r = r0 + 4 * rq;
+        if (c >= cols || r >= rows) continue;
+        const float4 o = make_float4(tile[4 * rq][oc], tile[4 * rq + 1][oc], tile[4 * rq + 2][oc], tile[4 * rq + 3][oc]);
+        float* dp = dst + c * ldd + r;
+        if (r + 3 < rows) {
+            *reinterpret_cast<float4*>(dp) = o;
+        } else {
+            dp[0] = o.x;
+            if (r + 1 < rows) dp[1] = o.y;
+            if (r + 2 < rows) dp[2] = o.z;
+        }
+    }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 __global__ void pad_rows_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, float* __restrict__ dst,
                                 int64_t ldd) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -611,6 +661,11 @@ int pick_bn(int64_t N, bool split3) {
 int launch_transpose(const float* src, int64_t rows, int64_t cols, int64_t lds, float* dst, int64_t ldd,
                      cudaStream_t s) {
     if (rows <= 0 || cols <= 0) return 0;
+    if (lds % 4 == 0 && ldd % 4 == 0 && aligned16(src) && aligned16(dst)) {
+        dim3 g((unsigned)((rows + 63) / 64), (unsigned)((cols + 63) / 64));
+        transpose64_kernel<false><<<g, 256, 0, s>>>(src, rows, cols, lds, nullptr, dst, ldd);
+        return 1;
+    }
     dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32));
     transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, lds, dst, ldd);
     return 1;
@@ -619,6 +674,11 @@ int launch_transpose(const float* src, int64_t rows, int64_t cols, int64_t lds, 
 int launch_relu_transpose(const float* Z, int64_t rows, int64_t cols, int64_t ldz, float* H, float* Ht,
                           int64_t ldt, cudaStream_t s) {
     if (rows <= 0) return 0;
+    if (ldz % 4 == 0 && ldt % 4 == 0 && aligned16(Z) && aligned16(H) && aligned16(Ht)) {
+        dim3 g((unsigned)((rows + 63) / 64), (unsigned)((ldz + 63) / 64));
+        transpose64_kernel<true><<<g, 256, 0, s>>>(Z, rows, cols, ldz, H, Ht, ldt);
+        return 1;
+    }
     dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((ldz + 31) / 32));
     relu_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(Z, rows, cols, ldz, H, Ht, ldt);
     return 1;

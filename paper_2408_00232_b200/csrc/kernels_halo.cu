@@ -726,14 +726,14 @@ __global__ void nvl_barrier_kernel(const __grid_constant__ BarTab t, uint64_t se
     const long long t0 = clock64();
     for (;;) {
         uint64_t v;
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(t.my_slots + j) : "memory");
+        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(t.my_slots + j) : "memory");
         if (v >= seq) break;
         if (clock64() - t0 > 20000000000LL) {   // ~10 s at 2 GHz: report, do not hang
             atomicExch(err, 5);
             break;
         }
-        __nanosleep(100);
     }
+    __threadfence_system();   // acquire: the peer's stores before its release are visible
 }
 
 // ---- dispatch by row width: LPR lanes x VPL float4 per lane cover ld columns ------
