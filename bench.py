@@ -173,6 +173,14 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
+def workload_config(cfgc, ds, args, world):
+    """The config keys both arms report (same workload, mode and partitioning)."""
+    return {"workload": f"{cfgc.key} {cfgc.name}: {ds.n} V, {2 * ds.m} CSR nnz, "
+                        f"dims {'-'.join(map(str, cfgc.dims))}",
+            "mode": args.mode, "partitions": world, "parallelism": f"vertex-cut p{world}",
+            "l2": "inputs larger than L2 (CSR %.2f GB, X %.2f GB)" % (2 * ds.m * 8 / 1e9, ds.X.nbytes / 1e9)}
+
+
 def reference_main(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -191,7 +199,9 @@ def reference_main(args):
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": args.config, "mode": "oracle p=1"},
+        "data": "synthetic", "config": {**workload_config(get_config(args.config), ds, args, args.gpus),
+                                        "oracle": "unpartitioned p=1 epoch, fp64 (the same Alg. 1 "
+                                                  "arithmetic in exact mode)"},
         "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": cpu_cores(), "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -390,13 +400,9 @@ def _main(args, real_stdout):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"{cfgc.key} {cfgc.name}: {ds.n} V, {2 * ds.m} CSR nnz, "
-                               f"dims {'-'.join(map(str, cfgc.dims))}",
-                   "mode": args.mode, "partitions": world, "parallelism": f"vertex-cut p{world}",
+        "config": {**workload_config(cfgc, ds, args, world),
                    "transport": ["none", "nccl", "nvlink-push"][stats[-1]["transport"]],
-                   "overlap": args.overlap and world > 1 and stats[-1]["transport"] != 1,
-                   "l2": "inputs larger than L2 (CSR %.2f GB, X %.2f GB)" %
-                         (2 * ds.m * 8 / 1e9, ds.X.nbytes / 1e9)},
+                   "overlap": args.overlap and world > 1 and stats[-1]["transport"] != 1},
         "comm_bytes_per_epoch": int(tot[0]), "comm_wire_bytes_per_epoch": int(tot[1]),
         "remote_accesses_per_epoch": int(tot[2]), "remote_accesses_baseline": int(tot[3]),
         "remote_accesses_avoided_frac": round(1 - tot[2] / tot[3], 4) if tot[3] else None,
