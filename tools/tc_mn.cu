@@ -35,5 +35,28 @@ int main(int argc, char** argv) {
     }
     printf("MN-major B (LBO %d SBO %d) M %d N %d K %d: rc=%d err=%s maxerr %g\n", GEMM_MN_LBO, GEMM_MN_SBO, M, N, K,
            rc, cudaGetErrorString(e), maxerr);
+    // production path: ∇W = Hᵀ S with H [K x M], S [K x N] row-major (both MN-major), 1x and 3xTF32
+    for (int split3 = 0; split3 < 2; ++split3) {
+        const int Mw = 602, Nw = 44, Kw = 5000, ldh = 604, lds = 44;
+        std::vector<float> H((size_t)Kw * ldh, 0.f), S((size_t)Kw * lds, 0.f), W((size_t)Mw * Nw);
+        for (int k = 0; k < Kw; ++k) for (int m = 0; m < Mw; ++m) H[(size_t)k * ldh + m] = (float)((k * 3 + m * 5) % 9 - 4) * 0.25f;
+        for (int k = 0; k < Kw; ++k) for (int n = 0; n < 41; ++n) S[(size_t)k * lds + n] = (float)((k * 7 + n * 2) % 5 - 2) * 0.5f;
+        float *dH, *dS, *dW, *dws;
+        const int64_t cap = 64LL * Mw * 48;
+        cudaMalloc(&dH, H.size() * 4); cudaMalloc(&dS, S.size() * 4); cudaMalloc(&dW, W.size() * 4); cudaMalloc(&dws, cap * 4);
+        cudaMemcpy(dH, H.data(), H.size() * 4, cudaMemcpyHostToDevice);
+        cudaMemcpy(dS, S.data(), S.size() * 4, cudaMemcpyHostToDevice);
+        int lc = 0;
+        int r2 = gemm_tc_wgrad_mn(Mw, Nw, Kw, dH, ldh, dS, lds, dW, Nw, dws, cap, false, split3 != 0, 0, &lc);
+        cudaError_t e2 = cudaDeviceSynchronize();
+        cudaMemcpy(W.data(), dW, W.size() * 4, cudaMemcpyDeviceToHost);
+        double me = 0; int nb = 0;
+        for (int m = 0; m < Mw; ++m) for (int n = 0; n < Nw; ++n) {
+            double r = 0; for (int k = 0; k < Kw; ++k) r += (double)H[(size_t)k * ldh + m] * S[(size_t)k * lds + n];
+            double d = fabs(r - W[(size_t)m * Nw + n]); if (d > me) me = d;
+            if (d > 1e-2 && nb < 4) { printf("  W[%d][%d]=%f ref %f\n", m, n, W[(size_t)m * Nw + n], r); nb++; }
+        }
+        printf("wgrad_mn split3=%d: rc=%d err=%s maxerr %g\n", split3, r2, cudaGetErrorString(e2), me);
+    }
     return 0;
 }
