@@ -210,8 +210,20 @@ __global__ void __launch_bounds__(256) loss_kernel(const float* __restrict__ log
 
 __global__ void reduce_rows_kernel(const float* __restrict__ x, int64_t n, double* out) {
     __shared__ double sh[1024];
+    // 8 independent loads in flight per thread; partial sums combined in a fixed order
+    constexpr int U = 8;
+    double acc[U] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int64_t step = (int64_t)blockDim.x * U;
+    for (int64_t i0 = threadIdx.x; i0 < n; i0 += step) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + (int64_t)u * blockDim.x;
+            if (i < n) acc[u] += (double)__ldg(x + i);
+        }
+    }
     double s = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += (double)x[i];
+#pragma unroll
+    for (int u = 0; u < U; ++u) s += acc[u];
     sh[threadIdx.x] = s;
     __syncthreads();
     for (int o = blockDim.x / 2; o > 0; o >>= 1) {
