@@ -869,6 +869,13 @@ int spmm_part(cdfgnn_ctx* c, LocalPart& P, const float* T, float* Y, int64_t ld,
 // the epoch.  Results agree with the per-epoch schedule up to fp32 rounding order.
 bool hoisted(const cdfgnn_ctx* c, int l) { return l == 1 && c->cfg.static_inputs == 2; }
 
+// ∇W from MN-major H and S in place (default) or from transposed K-major copies
+// (CDFGNN_WGRAD_KMAJOR=1, the earlier path)
+bool wgrad_mn() {
+    static const bool v = [] { const char* e = getenv("CDFGNN_WGRAD_KMAJOR"); return !(e && atoi(e) != 0); }();
+    return v;
+}
+
 int ensure_ax(cdfgnn_ctx* c, LocalPart& P, const float* X, int64_t ld_in, cudaStream_t s) {
     if (P.ax_src == X) return CDFGNN_OK;
     const int64_t F0 = c->cfg.dims[0];
@@ -881,7 +888,7 @@ int ensure_ax(cdfgnn_ctx* c, LocalPart& P, const float* X, int64_t ld_in, cudaSt
     launch_spmm(P.rowptr, P.colidx, P.val, S.n_items, spmm_items(P, 0, ld_in), X, P.ax, ld_in, s);
     c->launches++;
     CDF_TRY(check_launch("spmm (input aggregation)"));
-    if (P.xT) {
+    if (P.xT && !wgrad_mn()) {
         c->launches += launch_transpose(P.ax, P.n, F0, ld_in, P.xT, ld_of(P.n), s);
         P.xT_src = P.ax;
     }
@@ -933,7 +940,7 @@ int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, cons
         mark(c, PH_OTHER, s);
         for (int t = 0; t < c->k; ++t) {
             LocalPart& P = c->parts[t];
-            if (P.hT[l] && c->in_epoch) {
+            if (P.hT[l] && c->in_epoch && !wgrad_mn()) {
                 // ReLU fused with the transpose the next layer's ∇W needs (K-major Hᵀ)
                 c->launches += launch_relu_transpose(Z[t], P.n, Fo, ld_out, H_out[t], P.hT[l], ld_of(P.n), s);
                 P.hT_src[l] = H_out[t];
@@ -993,7 +1000,10 @@ int bwd_impl(cdfgnn_ctx* c, int l, float* const* dZ, int64_t ld, const float* co
         // dW (+)= H_inᵀ S ; parts accumulate in ascending order
         const float* Sg = hz ? dZ[t] : P.S;      // hoisted layer 1: (Â_i X_i)ᵀ δ^(1)
         const float* Hg = hz ? P.ax : H_in[t];
-        if (c->cfg.gemm_tf32) {
+        if (c->cfg.gemm_tf32 && wgrad_mn()) {
+            CDF_TRY(gemm_tc_wgrad_mn(Fi, Fo, P.n, Hg, ld_in, Sg, ld, dW, Fo, c->splitk, c->splitk_cap, t > 0,
+                                     c->cfg.gemm_tf32 == 3, s, &c->launches));
+        } else if (c->cfg.gemm_tf32) {
             const float* Ht = c->trA;
             int64_t ldh = c->npad;
             if (hz && P.xT) {

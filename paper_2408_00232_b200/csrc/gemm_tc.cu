@@ -3,9 +3,9 @@
 //   T  = H W                  (eq. 1; R5 Â(HW))        A = H,  B = Wᵀ (padded copy)
 //   δ̈  = (S Wᵀ) ⊙ 𝟙[H > 0]    (R3, R6)              A = S,  B = W  (padded copy)
 //   ∇W = Hᵀ S                 (eq. 5; R6), split-K  A = Hᵀ, B = Sᵀ (transposed copies)
-// Every operand is fed K-major: on sm_100a the tf32 MMA with an MN-major operand
-// descriptor returned zeros in our tests (tools/tc_debug.cu), so the two
-// vertex-major operands of ∇W are transposed into K-major scratch first.
+// T = HW and δ̈ feed K-major operands; ∇W reads H and S in place as MN-major operands, which
+// for tf32 the UMMA accepts only in the 128-B swizzle with 32-B atoms (layout type 1, 4 k-rows
+// per atom) — with the plain 128-B swizzle the accumulators came back zero.
 //
 // One CTA computes a 128 x BN fp32 tile over a K range: warp 0 issues TMA loads
 // (128-byte swizzled boxes, fp32 -> tf32 rounding in the tensor map) into a
@@ -38,7 +38,7 @@ constexpr int kThreads = 32 * (2 + kConvWarps + kEpiWarps);   // TMA, MMA, conve
 #define GEMM_MN_LBO (BK * 128)   // MN-major: byte stride between 32-element MN chunks
 #endif
 #ifndef GEMM_MN_SBO
-#define GEMM_MN_SBO 1024         // MN-major: byte stride between groups of 8 k-rows
+#define GEMM_MN_SBO 512          // MN-major: byte stride between groups of 4 k-rows (32-B-atom swizzle)
 #endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -110,15 +110,19 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uin
 }
 
 // 128-byte-swizzled shared-memory matrix descriptor (sm_100 UMMA, version 1)
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
     uint64_t d = 0;
     d |= (uint64_t)((addr & 0x3FFFFu) >> 4);
     d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
     d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
     d |= (uint64_t)1 << 46;          // descriptor version (sm_100)
-    d |= (uint64_t)2 << 61;          // SWIZZLE_128B
+    d |= (uint64_t)layout << 61;     // 2 = SWIZZLE_128B (K-major); 1 = SWIZZLE_128B_BASE32B (MN-major tf32)
     return d;
 }
+// MN-major tf32 operands: the only smem layout the UMMA accepts is 128-B swizzle with 32-B atoms
+// (CUTLASS sm100_common.inl), 4 k-rows per swizzle atom: SBO = 512 B, LBO = 4 KB between the
+// 32-wide MN chunks of a stage, +1024 B per 8 k-rows
+__device__ __forceinline__ uint64_t smem_desc_mn(uint32_t addr) { return smem_desc(addr, GEMM_MN_LBO, GEMM_MN_SBO, 1); }
 
 // 32 lanes x 32 consecutive 32-bit TMEM columns -> 32 registers per thread
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -296,10 +300,10 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         const uint32_t alo = a_base + C_::TMA_BYTES, blo = b_base + C_::TMA_BYTES;
 #pragma unroll
                         for (int kk = 0; kk < BK / 8; ++kk) {
-                            const uint64_t ah = smem_desc(a_base + kk * 32, 16, 1024);
-                            const uint64_t bh = smem_desc(b_base + kk * 32, 16, 1024);
-                            const uint64_t al = smem_desc(alo + kk * 32, 16, 1024);
-                            const uint64_t bl = smem_desc(blo + kk * 32, 16, 1024);
+                            const uint64_t ah = A_MN ? smem_desc_mn(a_base + kk * 1024) : smem_desc(a_base + kk * 32, 16, 1024);
+                            const uint64_t bh = B_MN ? smem_desc_mn(b_base + kk * 1024) : smem_desc(b_base + kk * 32, 16, 1024);
+                            const uint64_t al = A_MN ? smem_desc_mn(alo + kk * 1024) : smem_desc(alo + kk * 32, 16, 1024);
+                            const uint64_t bl = B_MN ? smem_desc_mn(blo + kk * 1024) : smem_desc(blo + kk * 32, 16, 1024);
                             tc_mma_tf32(dcol, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
                             tc_mma_tf32(dcol, ah, bl, idesc, 1u);
                             tc_mma_tf32(dcol, al, bh, idesc, 1u);
@@ -309,9 +313,9 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         for (int kk = 0; kk < BK / 8; ++kk) {
                             // K-major: +32 B per 8 tf32 inside the 128-B swizzle row (SBO = 8 rows)
                             // MN-major: +1024 B per 8 k-rows (LBO = stride of 32-wide MN chunks)
-                            const uint64_t ad = A_MN ? smem_desc(a_base + kk * 1024, GEMM_MN_LBO, GEMM_MN_SBO)
+                            const uint64_t ad = A_MN ? smem_desc_mn(a_base + kk * 1024)
                                                      : smem_desc(a_base + kk * 32, 16, 1024);
-                            const uint64_t bd = B_MN ? smem_desc(b_base + kk * 1024, GEMM_MN_LBO, GEMM_MN_SBO)
+                            const uint64_t bd = B_MN ? smem_desc_mn(b_base + kk * 1024)
                                                      : smem_desc(b_base + kk * 32, 16, 1024);
                             tc_mma_tf32(dcol, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
                         }
@@ -574,7 +578,7 @@ EncodeFn encode_fn() {
 
 // 2-D fp32 row-major matrix [rows x cols] with row stride ld (elements); box {bc, br}
 bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld, int bc, int br,
-              bool raw_fp32 = false) {
+              bool raw_fp32 = false, bool mn_major = false) {
     EncodeFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -582,7 +586,9 @@ bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int
     cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
     cuuint32_t es[2] = {1, 1};
     CUresult r = fn(m, raw_fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_TFLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -718,6 +724,33 @@ int gemm_tc_bwd_data(int64_t M, int64_t N, int64_t K, const float* A, int64_t ld
 }
 
 // C[M x N] (+)= Ht · Stᵀ with Ht = Hᵀ [M x K] (ldh) and St = Sᵀ [N x K] (lds), K = vertices; split-K
+// ∇W = Hᵀ S reading H [K x M] and S [K x N] in place as MN-major operands (128-B swizzle with
+// 32-B atoms, the layout the UMMA requires for MN-major tf32): no transposed copies
+int gemm_tc_wgrad_mn(int64_t M, int64_t N, int64_t K, const float* H, int64_t ldh, const float* S, int64_t lds,
+                     float* C, int64_t ldc, float* ws, int64_t ws_cap, bool accumulate, bool split3, cudaStream_t s,
+                     int* launches) {
+    const int BN = pick_bn(N, split3);
+    CUtensorMap ta, tb;
+    if (!make_map(&ta, H, K, M, ldh, 32, BK, split3, true) || !make_map(&tb, S, K, N, lds, 32, BK, split3, true))
+        CDF_FAIL(CDFGNN_ECUDA, "cuTensorMapEncodeTiled failed (wgrad, MN-major)");
+    const int64_t ldw = (N + 3) / 4 * 4;
+    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    const int64_t total_kb = (K + BK - 1) / BK;
+    int64_t splits = std::max<int64_t>(1, std::min<int64_t>(2 * 148 / std::max<int64_t>(tiles, 1), total_kb / 8));
+    while (splits > 1 && splits * M * ldw > ws_cap) splits--;
+    const int kbps = (int)((total_kb + splits - 1) / splits);
+    const int zs = (int)((total_kb + kbps - 1) / kbps);
+    EpiArgs ep{nullptr, 0, nullptr, 0, ws, ldw, 0, 0};
+    CUtensorMap tc;
+    ep.tma = make_store_map(&tc, ws, M, ldw, ldw, zs, true) ? 1 : 0;
+    int rc = launch_bn<true, true>(BN, split3, ta, tb, tc, M, N, K, (int)splits, ep, s);
+    if (rc != CDFGNN_OK) CDF_FAIL(rc, "wgrad launch failed");
+    const int64_t tot = M * ldc;
+    splitk_sum_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(M, N, ldw, zs, ws, C, ldc, accumulate ? 1 : 0);
+    if (launches) *launches += 2;
+    return cudaGetLastError() == cudaSuccess ? CDFGNN_OK : CDFGNN_ECUDA;
+}
+
 int gemm_tc_wgrad(int64_t M, int64_t N, int64_t K, const float* Ht, int64_t ldh, const float* St, int64_t lds,
                   float* C, int64_t ldc, float* ws, int64_t ws_cap, bool accumulate, bool split3, cudaStream_t s,
                   int* launches) {

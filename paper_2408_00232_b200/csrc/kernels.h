@@ -147,6 +147,9 @@ int gemm_tc_wgrad(int64_t M, int64_t N, int64_t K, const float* Ht, int64_t ldh,
                   cudaStream_t s, int* launches);
 // out[k] = X[idx[k]] rows (ld floats, ld % 4 == 0), k < count; returns the launch count
 int launch_gather_rows(const float* X, int64_t ld, const int32_t* idx, int64_t count, float* out, cudaStream_t s);
+int gemm_tc_wgrad_mn(int64_t M, int64_t N, int64_t K, const float* H, int64_t ldh, const float* S, int64_t lds,
+                     float* C, int64_t ldc, float* ws, int64_t ws_cap, bool accumulate, bool split3,
+                     cudaStream_t s, int* launches);
 void launch_read_probe(const float4* p, int64_t n4, int reps, float* sink, cudaStream_t s);
 void launch_relu(const float* Z, float* H, int64_t count, cudaStream_t s);
 void launch_loss(const float* logits, int64_t ld, int C, int64_t n, int64_t B, int64_t M,
