@@ -45,7 +45,12 @@ def parse():
                     help="1: also time the hoisted-input-aggregation schedule (static_inputs = 2) and "
                          "report it under 'hoisted' (the headline keeps the per-epoch schedule)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-frac", type=float, default=0.01)
+    ap.add_argument("--ref-budget", type=float, default=200.0,
+                    help="--impl reference: seconds of whole oracle epochs (at least one runs)")
+    ap.add_argument("--coresident", type=int, default=4,
+                    help="N = 1 only: also time the same workload as this many co-resident partitions "
+                         "on the one GPU (whole method incl. the halo exchange), reported under "
+                         "'coresident_p<k>'; 0 = off")
     ap.add_argument("--scale", type=float, default=None, help="shrink the graph (tests only)")
     return ap.parse_args()
 
@@ -120,50 +125,25 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle leg
-class OracleSample:
-    """Estimated ms of one oracle epoch (oracle/gcn.py, fp64, p = 1) on this host.
+class OracleEpoch:
+    """Whole epochs of the CPU oracle (oracle/gcn.py train_step: the plain unpartitioned
+    full-batch GCN epoch in fp64, P:L236-283 — forward, loss, backward with every SpMM at
+    full size; scipy CSR x dense is single-threaded, numpy BLAS uses the host's cores).
+    Â and the fp64 operands are built once, outside the timing."""
 
-    Sample: every dense op (GEMMs, ReLU, loss) runs at full size on operands of the
-    right shape; each SpMM (scipy CSR, single-threaded) runs on a random `frac` row
-    sample of Â and is scaled by 1/frac.  Â is built once, outside the timing."""
-
-    def __init__(self, ds, frac):
+    def __init__(self, ds):
         import numpy as np
         from oracle.graph import normalized_adjacency
-        self.ds, self.frac = ds, frac
+        self.ds = ds
         self.A = normalized_adjacency(ds.n, ds.eu, ds.ev)
         self.W = [w.astype(np.float64) for w in ds.W]
         self.X = ds.X.astype(np.float64)
 
-    def epoch_ms(self, seed=0):
-        import numpy as np
+    def epoch_ms(self):
         from oracle import gcn
-        ds, frac, W = self.ds, self.frac, self.W
-        rng = np.random.default_rng(seed)
-        rows = np.sort(rng.choice(ds.n, max(1, int(frac * ds.n)), replace=False))
-        As = self.A[rows]
-        L = len(W)
-        t_dense = 0.0
-        t_spmm = 0.0
-        H = [self.X]
-        for l in range(1, L + 1):
-            t0 = time.perf_counter(); T = H[l - 1] @ W[l - 1]; t_dense += time.perf_counter() - t0
-            t0 = time.perf_counter(); _ = As @ T; t_spmm += time.perf_counter() - t0
-            t0 = time.perf_counter(); Hn = gcn.relu(T) if l < L else T
-            t_dense += time.perf_counter() - t0
-            H.append(Hn)
         t0 = time.perf_counter()
-        _, delta, _ = gcn.loss_grad(H[L], ds.y, ds.train)
-        t_dense += time.perf_counter() - t0
-        for l in range(L, 0, -1):
-            t0 = time.perf_counter(); _ = As @ delta; t_spmm += time.perf_counter() - t0
-            S = delta                                   # full-size stand-in of Â δ
-            t0 = time.perf_counter()
-            _ = H[l - 1].T @ S
-            if l > 1:
-                delta = (S @ W[l - 1].T) * (H[l - 1] > 0)
-            t_dense += time.perf_counter() - t0
-        return 1e3 * (t_dense + t_spmm / frac)
+        gcn.train_step(self.A, self.X, self.W, self.ds.y, self.ds.train)
+        return 1e3 * (time.perf_counter() - t0)
 
 
 def cpu_cores():
@@ -182,28 +162,38 @@ def workload_config(cfgc, ds, args, world):
 
 
 def reference_main(args):
+    """--impl reference: the oracle (this tier's reference arm) as it stands, whole epochs of
+    the same workload on the host's cores.  A C3 epoch takes ~1-1.5 min, so the arm runs
+    whole epochs until --ref-budget seconds are spent (at least one) and reports the epochs it
+    actually executed (`steps`; the request is `steps_requested`); no warm-up epochs (the
+    first epoch is timed like the others)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     from synth import get_config
     from synth.cache import cached_dataset
     ds = cached_dataset(get_config(args.config), args.scale)
-    orc = OracleSample(ds, args.cpu_frac)
-    for _ in range(args.warmup):
-        orc.epoch_ms(seed=1)
-    vals = [orc.epoch_ms(seed=2 + k) for k in range(args.steps)]
+    orc = OracleEpoch(ds)
+    vals = []
+    t0 = time.time()
+    while len(vals) < args.steps and (not vals or time.time() - t0 + vals[-1] / 1e3 <= args.ref_budget):
+        vals.append(orc.epoch_ms())
     v = statistics.mean(vals)
-    sample = (f"oracle epoch (oracle/gcn.py fp64, p=1) on {args.config}: dense ops full size, "
-              f"each SpMM on a {args.cpu_frac:.0%} row sample scaled by {1 / args.cpu_frac:.0f}")
+    sample = (f"{len(vals)} whole oracle epoch(s) (oracle/gcn.py train_step, fp64, p=1, unpartitioned "
+              f"full-batch GCN at full size) on {args.config}; scipy CSR SpMM single-threaded, numpy BLAS "
+              f"on the host's cores; budget {args.ref_budget:.0f} s, no warm-up")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 3),
+        "n_gpus": args.gpus, "steps": len(vals), "steps_requested": args.steps, "steps_executed": len(vals),
+        "warmup": 0, "warmup_requested": args.warmup, "ms_per_step": round(v, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {**workload_config(get_config(args.config), ds, args, args.gpus),
-                                        "oracle": "unpartitioned p=1 epoch, fp64 (the same Alg. 1 "
-                                                  "arithmetic in exact mode)"},
+                                        "oracle": "unpartitioned p=1 epoch, fp64 (the plain definition "
+                                                  "Alg. 1 reduces to at eps=0 without quantisation)"},
+        "note": (f"{args.steps} oracle epochs would take ~{args.steps * v / 6e4:.0f} min; "
+                 f"{len(vals)} executed") if len(vals) < args.steps else "",
         "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": cpu_cores(), "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, "epochs": [round(x, 1) for x in vals]},
         "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
     return 0
@@ -226,6 +216,55 @@ def main(args):
         os.close(real_stdout)
 
 
+# ------------------------------------------------------------------ halo accounting
+def sync_schedule(L, elide=True):
+    """(direction, l, gather ran, scatter ran) of the 2L syncs of one cdfgnn_epoch (§8 f2:
+    the layer-L forward scatter and backward gather are elided)."""
+    out = [("fwd", l, True, not (elide and l == L)) for l in range(1, L + 1)]
+    out += [("bwd", l, not (elide and l == L), True) for l in range(L, 0, -1)]
+    return out
+
+
+def msg_bytes(F, B):
+    """Algorithmic bytes of one vertex message (O9 / R25): B-bit codes + lo, hi + position."""
+    return (B * F + 7) // 8 + 12 if B else 4 * F + 4
+
+
+def remote_split(st, M, L, elide=True):
+    """R25: one remote access = one replica -> replica vertex message; the uncached baseline is
+    2M per sync.  Split of the avoided ones into dead-sync elision (§8 f2) and the cache."""
+    base = 4 * L * M
+    sent = sum(s["gather_sent"] + s["scatter_msgs"] for s in st["fwd"] + st["bwd"])
+    elided = sum((not g) * M + (not sc) * M for _, _, g, sc in sync_schedule(L, elide))
+    cache = base - sent - elided
+    return {"baseline": base, "sent": sent, "avoided_by_cache": cache, "avoided_by_elision": elided,
+            "avoided_frac": round(1 - sent / base, 4) if base else None,
+            "avoided_frac_cache": round(cache / base, 4) if base else None,
+            "avoided_frac_elision": round(elided / base, 4) if base else None}
+
+
+def halo_bytes(st, dims, M, B, quant, cache=True, elide=True):
+    """Algorithmic HBM bytes of the three halo kernels in one epoch, summed over
+    the executed syncs: gather (a3+a4: read z, s of every mirror row = 8F; per sender the
+    snapshot write 4F and the message), master (a6+a7: read a, z, s, b = 16F and the received
+    messages; write the Z row 4F, a and b 8F per active master, s 4F per fired master, the
+    scatter messages), mirror (read b 4F + the message per received row; write b 4F per message,
+    the Z row 4F)."""
+    L = len(dims) - 1
+    g = m = r = 0
+    for d, l, gran, sran in sync_schedule(L, elide):
+        s = st[d][l - 1]
+        F = dims[l]
+        mb = msg_bytes(F, quant)
+        if gran:
+            g += (8 if cache else 4) * F * M + s["gather_sent"] * ((4 * F if cache else 0) + mb)
+        m += (16 if cache else 4) * F * B + s["gather_sent"] * mb + 4 * F * B
+        m += (s["active"] * 8 * F + s["master_fired"] * 4 * F if cache else 0) + s["scatter_msgs"] * mb
+        if sran:
+            r += (4 * F * M if cache else 0) + s["scatter_msgs"] * (mb + (4 * F if cache else 0)) + 4 * F * M
+    return {"gather": g, "master": m, "mirror": r}
+
+
 def _main(args, real_stdout):
     import numpy as np
     import torch
@@ -246,35 +285,16 @@ def _main(args, real_stdout):
         dist.barrier()
     if rank != 0:
         ds = cached_dataset(cfgc, args.scale, wait_for_writer=True, write=False)
-    mode = {"cache_int8": (True, 8), "cache_fp32": (True, 0), "quant_only": (False, 8),
-            "nocache": (False, 0)}[args.mode]
-    run = Run(ds, world, rank=rank, world=world, device=local, cache=mode[0], quant_bits=mode[1],
-              eps0=args.eps0, adaptive=True, optimizer="adam", lr=0.01, timing=True,
-              host_inputs=not args.no_e2e, transport=args.transport, static_inputs=True,
-              overlap=args.overlap)
+    cache_on, quant = {"cache_int8": (True, 8), "cache_fp32": (True, 0), "quant_only": (False, 8),
+                       "nocache": (False, 0)}[args.mode]
+    common = dict(cache=cache_on, quant_bits=quant, eps0=args.eps0, adaptive=True, optimizer="adam",
+                  lr=0.01, timing=True, transport=args.transport, overlap=args.overlap)
+    run = Run(ds, world, rank=rank, world=world, device=local, host_inputs=not args.no_e2e,
+              static_inputs=True, **common)
     t_prep = time.time() - t_prep
-    for _ in range(args.warmup):
-        run.epoch()
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    clocks = ClockSampler(local) if rank == 0 else None
-    if clocks:
-        clocks.start()
     stream = torch.cuda.current_stream()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    e0.record(stream)
-    stats = [run.epoch() for _ in range(args.steps)]
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    clk = clocks.stop() if clocks else None
-    ms = e0.elapsed_time(e1) / args.steps
 
     def allred(vals, op):
         t = torch.tensor(vals, dtype=torch.float64, device="cuda")
@@ -284,57 +304,66 @@ def _main(args, real_stdout):
 
     sumop = dist.ReduceOp.SUM if dist else None
     maxop = dist.ReduceOp.MAX if dist else None
-    ms_max = allred([ms], maxop)[0]
+
+    def timed(step_fn, sampler=None):
+        """W untimed warm-ups, then K steps between CUDA events on the launching stream, with a
+        barrier + synchronize on both sides; returns (max-over-ranks ms per step, stats)."""
+        for _ in range(args.warmup):
+            step_fn()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        if sampler:
+            sampler.start()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        e0.record(stream)
+        out = [step_fn(k) for k in range(args.steps)]
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        clk = sampler.stop() if sampler else None
+        return allred([e0.elapsed_time(e1) / args.steps], maxop)[0], out, clk
+
+    clocks = ClockSampler(local) if rank == 0 else None
+    ms_max, stats, clk = timed(lambda k=0: run.epoch(), clocks)
+    avg = lambda key: sum(st[key] for st in stats) / args.steps
     comm_alg = sum(sum(s["bytes_alg"] for s in st["fwd"] + st["bwd"]) for st in stats) / args.steps
     comm_wire = sum(sum(s["bytes_wire"] for s in st["fwd"] + st["bwd"]) for st in stats) / args.steps
-    remote = sum(sum(s["gather_sent"] + s["scatter_msgs"] for s in st["fwd"] + st["bwd"])
-                 for st in stats) / args.steps
-    base = sum(sum(s["baseline"] for s in st["fwd"] + st["bwd"]) for st in stats) / args.steps
-    sp_bytes = sum(st["spmm_bytes"] for st in stats)
+    M_loc = sum(v["n_mirror"] for v in run.views)
+    rsplit = [remote_split(st, M_loc, run.cfg.L) for st in stats]
+    rs_keys = ("baseline", "sent", "avoided_by_cache", "avoided_by_elision")
+    rs_tot = allred([sum(r[k] for r in rsplit) / args.steps for k in rs_keys], sumop)
+    sync_sub = [round(sum(st["ms_sync_sub"][i] for st in stats) / args.steps, 3) for i in range(6)]
+    tot = allred([comm_alg, comm_wire], sumop)
+    max_wire = allred([comm_wire], maxop)[0]
+    ms_sync_max = allred([avg("ms_sync")], maxop)[0]
+    launches = sum(st["gpu_launches"] for st in stats)
     sp_ms = sum(st["spmm_ms_sum"] for st in stats)
     sp_n = sum(st["spmm_launches"] for st in stats)
-    ms_sync = sum(st["ms_sync"] for st in stats) / args.steps
-    ms_spmm = sum(st["ms_spmm"] for st in stats) / args.steps
-    ms_gemm = sum(st["ms_gemm"] for st in stats) / args.steps
-    sync_sub = [round(sum(st["ms_sync_sub"][i] for st in stats) / args.steps, 3) for i in range(6)]
-    tot = allred([comm_alg, comm_wire, remote, base], sumop)
-    max_wire = allred([comm_wire], maxop)[0]
-    ms_sync_max = allred([ms_sync], maxop)[0]
-    launches = sum(st["gpu_launches"] for st in stats)
+    sp_comp = sum(st["spmm_bytes_compulsory"] for st in stats)
+    sp_gather = sum(st["spmm_bytes"] for st in stats)
+    sp_ld = stats[-1]["spmm_ld"]
     # ---- end to end through the public API with host inputs (pinned), copies inside the region
     e2e = None
     if not args.no_e2e:
-        def timed_host_loop(pipelined):
-            if pipelined:
-                run.epoch_host_next(prefetch_next=False)
-            else:
-                run.epoch_host()
-            torch.cuda.synchronize()
-            if dist is not None:
-                dist.barrier()
-            e0.record(stream)
-            for k in range(args.steps):
-                if pipelined:
-                    # step k's inputs were copied under step k-1 (step 0 copies its own inside the
-                    # region); step k starts the copy of step k+1's — all K copies are timed
-                    run.epoch_host_next(prefetch_next=k + 1 < args.steps)
-                else:
-                    run.epoch_host()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            if dist is not None:
-                dist.barrier()
-            return allred([e0.elapsed_time(e1) / args.steps], maxop)[0]
-        e2e_serial_ms = timed_host_loop(False)
-        e2e_ms = timed_host_loop(True)
-        # bytes the pipelined host path copies per step: at N > 1 only each part's owned X rows
-        # (its M mirror rows arrive from their masters over NVLink), plus labels and masks
+        def host_step(pipelined):
+            def f(k=None):
+                if not pipelined:
+                    return run.epoch_host()
+                # step k's inputs were copied under step k-1 (the first timed step copies its
+                # own inside the region); step k starts the copy of step k+1's
+                return run.epoch_host_next(prefetch_next=k is not None and k + 1 < args.steps)
+            return f
+        e2e_serial_ms = timed(host_step(False))[0]
+        e2e_ms = timed(host_step(True))[0]
         h2d = 0
         for pv, x, y, m in zip(run.views, run.X_host, run.labels_host, run.masks_host):
             owned = pv["n_local"] - (pv["n_mirror"] if world > 1 else 0)
             h2d += owned * x.shape[1] * x.element_size() + y.numel() * y.element_size() + m.numel() * m.element_size()
-        k = len(run.parts)
-        d2h = 8 * k + 8 + 8 * 4 * 2 * run.cfg.L
+        d2h = 8 * len(run.parts) + 8 + 8 * 4 * 2 * run.cfg.L
         h2d_all = allred([h2d, d2h], sumop)
         e2e = {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": int(h2d_all[0]),
                "d2h_bytes_per_step": int(h2d_all[1]),
@@ -345,26 +374,14 @@ def _main(args, real_stdout):
     run.close()
     plan = run.plan
     run.workspace = None
-    # ---- the same workload with the layer-1 aggregation hoisted (static_inputs = 2): Â_i X_i is
-    # built once per X buffer, layer 1 runs (Â_i X_i) W^(0) and ∇W^(0) = (Â_i X_i)ᵀ δ^(1)
+    peaks, src = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
+    # ---- the same workload with the layer-1 aggregation hoisted (static_inputs = 2)
     hoist = None
     if args.hoisted:
-        run2 = Run(ds, world, rank=rank, world=world, device=local, cache=mode[0], quant_bits=mode[1],
-                   eps0=args.eps0, adaptive=True, optimizer="adam", lr=0.01, timing=True,
-                   host_inputs=False, transport=args.transport, static_inputs=2, overlap=args.overlap,
-                   plan=plan)
-        for _ in range(args.warmup):
-            run2.epoch()
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-        e0.record(stream)
-        st2 = [run2.epoch() for _ in range(args.steps)]
-        e1.record(stream)
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-        h_ms = allred([e0.elapsed_time(e1) / args.steps], maxop)[0]
+        run2 = Run(ds, world, rank=rank, world=world, device=local, host_inputs=False, static_inputs=2,
+                   plan=plan, **common)
+        h_ms, st2, _ = timed(lambda k=0: run2.epoch())
         hoist = {"value": round(h_ms, 3), "unit": "ms", "loss": st2[-1]["loss"],
                  "gpu_launches": sum(x["gpu_launches"] for x in st2),
                  "phase_ms": {k: round(sum(x["ms_" + k] for x in st2) / args.steps, 3)
@@ -373,6 +390,51 @@ def _main(args, real_stdout):
                              "= (A_i X_i) W0, dW0 = (A_i X_i)^T delta1; same method, both layer-1 "
                              "SpMMs leave the epoch"}
         run2.close()
+        run2.workspace = None
+    # ---- N = 1: the whole method on one GPU — k co-resident vertex-cut partitions (cache test,
+    # quantise + pack, exchange and apply run on every boundary vertex; world = 1 transport)
+    cores = None
+    if world == 1 and args.coresident > 1:
+        k = args.coresident
+        run3 = Run(ds, k, host_inputs=False, static_inputs=True, **common)
+        c_ms, st3, _ = timed(lambda i=0: run3.epoch())
+        Mk = sum(v["n_mirror"] for v in run3.views)
+        Bk = sum(v["n_bmaster"] for v in run3.views)
+        hb = [halo_bytes(x, ds.dims, Mk, Bk, quant, cache_on) for x in st3]
+        sub = [sum(x["ms_sync_sub"][i] for x in st3) / args.steps for i in range(6)]
+        names = ("gather", "master", "mirror")
+        ms_of = {"gather": sub[0], "master": sub[2] + sub[3], "mirror": sub[5]}
+        kern = {}
+        for nm in names:
+            b = sum(h[nm] for h in hb) / args.steps
+            t = ms_of[nm]
+            kern[nm] = {"ms": round(t, 3), "bytes": int(b),
+                        "gbs": round(b / (t * 1e-3) / 1e9, 1) if t > 0 else None,
+                        "frac_hbm": round(b / (t * 1e-3) / 1e9 / hbm, 4) if t > 0 else None}
+        rs3 = [remote_split(x, Mk, run3.cfg.L) for x in st3]
+        cores = {
+            "value": round(c_ms, 3), "unit": "ms", "partitions": k,
+            "rf": round(sum(v["n_local"] for v in run3.views) / ds.n, 3),
+            "mirrors": Mk, "boundary_masters": Bk,
+            "phase_ms": {"gemm": round(sum(x["ms_gemm"] for x in st3) / args.steps, 3),
+                         "spmm": round(sum(x["ms_spmm"] for x in st3) / args.steps, 3),
+                         "sync": round(sum(x["ms_sync"] for x in st3) / args.steps, 3),
+                         "sync_split": dict(zip(["gather_pack", "gather_xfer", "master_apply",
+                                                 "scatter_pack", "scatter_xfer", "mirror_apply"],
+                                                [round(x, 3) for x in sub]))},
+            "halo_kernels": kern,
+            "bytes_model": "SURVEY 8(d3) algorithmic bytes of the executed syncs (bench.halo_bytes) / "
+                           "CUDA-event phase time / MEASURED_PEAKS hbm_gbs",
+            "comm_bytes_per_epoch": int(sum(sum(s["bytes_alg"] for s in x["fwd"] + x["bwd"]) for x in st3)
+                                        / args.steps),
+            "remote_accesses": {kk: (round(sum(r[kk] for r in rs3) / args.steps)
+                                     if not kk.startswith("avoided_frac") else rs3[-1][kk])
+                                for kk in rs3[-1]},
+            "loss": st3[-1]["loss"], "train_acc": st3[-1]["acc"], "eps": st3[-1]["eps_used"],
+            "gpu_launches": sum(x["gpu_launches"] for x in st3),
+            "transport": "co-resident, slot-addressed messages"}
+        run3.close()
+        run3.workspace = None
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -382,12 +444,10 @@ def _main(args, real_stdout):
     probe = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
     l2_gbs = bandwidth_probe(probe, 64 << 20, 64)
     del probe
-    peaks, src = measured_peaks()
-    hbm = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
-    sp_ld = stats[-1]["spmm_ld"]
-    sp_c = sum(st["spmm_bytes_compulsory"] for st in stats)
-    achieved = (sp_bytes / (sp_ms * 1e-3) / 1e9) if sp_ms > 0 else None
     avg_launch_ms = sp_ms / sp_n if sp_n else None
+    comp_per = sp_comp / sp_n if sp_n else None
+    gath_per = sp_gather / sp_n if sp_n else None
+    achieved = comp_per / (avg_launch_ms * 1e-3) / 1e9 if avg_launch_ms else None
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -395,6 +455,8 @@ def _main(args, real_stdout):
             traffic = json.load(open(tpath)).get(f"{args.config}_p{world}_{args.mode}_spmm_ld{sp_ld}")
         except Exception:
             traffic = None
+    frac = achieved / hbm if achieved else None
+    assert frac is None or frac <= 1.2, "compulsory-byte HBM fraction above 1.2: byte model is wrong"
     out = {
         "metric": METRIC, "value": round(ms_max, 3), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 3),
@@ -404,28 +466,37 @@ def _main(args, real_stdout):
                    "transport": ["none", "nccl", "nvlink-push"][stats[-1]["transport"]],
                    "overlap": args.overlap and world > 1 and stats[-1]["transport"] != 1},
         "comm_bytes_per_epoch": int(tot[0]), "comm_wire_bytes_per_epoch": int(tot[1]),
-        "remote_accesses_per_epoch": int(tot[2]), "remote_accesses_baseline": int(tot[3]),
-        "remote_accesses_avoided_frac": round(1 - tot[2] / tot[3], 4) if tot[3] else None,
+        "remote_accesses": dict(zip(rs_keys, [int(x) for x in rs_tot]),
+                                avoided_frac=round(1 - rs_tot[1] / rs_tot[0], 4) if rs_tot[0] else None,
+                                avoided_frac_cache=round(rs_tot[2] / rs_tot[0], 4) if rs_tot[0] else None,
+                                avoided_frac_elision=round(rs_tot[3] / rs_tot[0], 4) if rs_tot[0] else None),
         "nvlink": {"max_wire_bytes_per_gpu": int(max_wire), "sync_ms": round(ms_sync_max, 3),
                    "frac_of_900": round(max_wire / (ms_sync_max * 1e-3) / 1e9 / NVLINK_GBS, 4)
                    if ms_sync_max > 0 and max_wire > 0 else None},
-        "phase_ms": {"gemm": round(ms_gemm, 3), "spmm": round(ms_spmm, 3), "sync": round(ms_sync, 3),
+        "phase_ms": {"gemm": round(avg("ms_gemm"), 3), "spmm": round(avg("ms_spmm"), 3),
+                     "sync": round(avg("ms_sync"), 3),
                      "sync_split": dict(zip(["gather_pack", "gather_xfer", "master_apply",
                                              "scatter_pack", "scatter_xfer", "mirror_apply"], sync_sub))},
         "loss": stats[-1]["loss"], "train_acc": stats[-1]["acc"], "eps": stats[-1]["eps_used"],
         "roofline": {"kernel": f"spmm (ld={sp_ld}, the dominant launch group)", "bound": "hbm",
                      "achieved": round(achieved, 1) if achieved else None, "peak": hbm,
-                     "unit": "GB/s", "frac": round(achieved / hbm, 4) if achieved else None,
+                     "unit": "GB/s", "frac": round(frac, 4) if frac else None,
                      "traffic": traffic, "peak_source": src,
-                     "bytes_model": "gather model per launch: 4(n+1) + 8 nnz + 4 ld nnz + 4 ld n",
-                     "bytes_per_launch": round(sp_bytes / sp_n) if sp_n else None,
-                     "compulsory_bytes_per_launch": round(sp_c / sp_n) if sp_n else None,
+                     "bytes_model": "compulsory bytes per launch (SURVEY 8(d3)): 4(n+1) + 8 nnz "
+                                    "(rowptr, colidx, val) + 4 ld n (T) + 4 ld n (Z)",
+                     "bytes_per_launch": round(comp_per) if comp_per else None,
                      "avg_launch_ms": round(avg_launch_ms, 4) if avg_launch_ms else None,
+                     "launches": sp_n,
                      "dram_gbs": round(traffic / (avg_launch_ms * 1e-3) / 1e9, 1)
                      if (traffic and avg_launch_ms) else None,
+                     "gather_model_bytes_per_launch": round(gath_per) if gath_per else None,
+                     "l2_to_sm_gbs": round(gath_per / (avg_launch_ms * 1e-3) / 1e9, 1) if avg_launch_ms else None,
                      "l2_read_gbs_probe": round(l2_gbs, 1),
-                     "frac_of_l2": round(achieved / l2_gbs, 4) if achieved else None,
-                     "launches": sp_n},
+                     "frac_of_l2_probe": round(gath_per / (avg_launch_ms * 1e-3) / 1e9 / l2_gbs, 4)
+                     if avg_launch_ms else None,
+                     "note": "frac = compulsory HBM bytes / launch time / measured HBM peak; the kernel "
+                             "re-reads neighbour rows of T from L2 (gather model 4 ld nnz), so its "
+                             "ceiling is L2->SM delivery (l2_to_sm_gbs vs l2_read_gbs_probe)"},
         "gpu_launches": launches,
         "prep_s": round(t_prep, 1),
     }
@@ -433,15 +504,17 @@ def _main(args, real_stdout):
         out["e2e"] = e2e
     if hoist:
         out["hoisted"] = hoist
+    if cores:
+        out[f"coresident_p{args.coresident}"] = cores
     if clk:
         out["clocks"] = clk
     if world == 1 and not args.no_cpu_baseline:
-        v = OracleSample(ds, args.cpu_frac).epoch_ms()
+        orc = OracleEpoch(ds)
+        v = orc.epoch_ms()
         out["cpu_baseline"] = {
             "value": round(v, 1), "unit": "ms", "cores": cpu_cores(), "kind": "oracle",
-            "sample": f"oracle/gcn.py epoch (fp64, p=1): dense ops full size, each SpMM on a "
-                      f"{args.cpu_frac:.0%} row sample scaled by {1 / args.cpu_frac:.0f} "
-                      f"(scipy CSR single-threaded, numpy BLAS multi-threaded)"}
+            "sample": f"1 whole oracle epoch (oracle/gcn.py train_step, fp64, p=1, full {args.config}): "
+                      f"scipy CSR SpMM single-threaded, numpy BLAS on the host's cores"}
     sys.stdout.flush()
     os.write(real_stdout, (json.dumps(out) + "\n").encode())
     if dist is not None:

@@ -139,7 +139,11 @@ typedef struct {
     int32_t adaptive;                   /* 1: ε controller P:L386-399 */
     double mu1, mu2, nu1, nu2, xi, lam1, lam2;  /* P:L399 defaults */
     int32_t eps_clamp;                  /* 1: clamp ε to [ν2, ν1] (reading R17) */
-    int32_t quant_bits;                 /* 0 (fp32 payloads) or 8 (uint8 codes), §5 */
+    int32_t quant_bits;                 /* B of §5 (B is left free by the paper):
+                                           0 = fp32 payloads; 4, 8 (default) or 16-bit codes
+                                           (reading R15; code rows: B = 8 one byte per code,
+                                           B = 4 two per byte — code k in the low nibble of byte
+                                           k/2 for even k —, B = 16 little-endian uint16) */
     int32_t optimizer;                  /* 0 SGD, 1 Adam */
     double lr, beta1, beta2, adam_eps;
     int32_t gemm_tf32;                  /* 3: tcgen05 3xTF32 GEMMs (default, ~fp32 accuracy);
@@ -172,6 +176,18 @@ typedef struct {
                                            0 (default): measured slower on B200 — the
                                            split SpMM and the concurrent streaming kernels cost more
                                            L2 bandwidth than the hidden gather saves */
+    int32_t msg_layout;                 /* message regions: 0 (default) = slot-addressed for
+                                           co-resident parts and the NVLink push transport,
+                                           compacted for NCCL send/recv; 1 = compacted always
+                                           (per-peer packed buffers: ballot + prefix compaction,
+                                           counts, index maps, a copy kernel for push);
+                                           2 = slot-addressed (EUSAGE with transport = 1).
+                                           Slot-addressed: the message of the vertex at
+                                           halo-list position k lives in slot k of the (source,
+                                           destination) region — header {u32 stamp, f32 lo,
+                                           f32 hi, u32 0} + code row — stamped with the phase's
+                                           sequence number; senders store straight into the
+                                           receiver's region (through CUDA IPC on a peer GPU) */
 } cdfgnn_cfg;
 
 int cdfgnn_cfg_default(cdfgnn_cfg* cfg);
@@ -200,9 +216,11 @@ typedef struct {
     int64_t active;             /* active masters (Alg. 2 L12, L18) */
     int64_t scatter_msgs;       /* master -> mirror messages */
     int64_t baseline;           /* 2 M: messages without the cache */
-    int64_t bytes_alg;          /* (F+12) per int8 message, 4F+4 per fp32 message */
+    int64_t bytes_alg;          /* ceil(B·F/8) + 12 per B-bit message (F+12 at B = 8: codes,
+                                   lo, hi and a 32-bit position), 4F+4 per fp32 message */
     int64_t bytes_wire;         /* bytes that crossed to another GPU (NCCL payloads or
-                                   NVLink stores); 0 for co-resident partitions */
+                                   NVLink stores: 16-byte header + code row per message in the
+                                   slot layout); 0 for co-resident partitions */
 } cdfgnn_sync_stats;
 
 /* One gather + scatter synchronisation of layer l (1..L), direction dir
@@ -296,10 +314,41 @@ int cdfgnn_cache_view(cdfgnn_ctx* ctx, int32_t local_part, int32_t l, int32_t di
  *                     value the optimizer consumed; [F_{l-1} x F_l] row-major (ld = F_l). */
 int cdfgnn_act_view(cdfgnn_ctx* ctx, int32_t local_part, int32_t l, float** ptr, int64_t* rows, int64_t* ld);
 int cdfgnn_grad_view(cdfgnn_ctx* ctx, int32_t l, float** ptr, int64_t* rows, int64_t* ld);
-/* which: 0 gather-sent flag per mirror row, 1 master-fired flag, 2 active flag
- * (uint8 per row, of the most recent synchronisation). */
-int cdfgnn_sync_flags(cdfgnn_ctx* ctx, int32_t local_part, int32_t which, uint8_t** ptr,
-                      int64_t* rows);
+/* Cache-test decisions of the most recent synchronisation of layer l (1..L), direction dir
+ * (0 = Z, 1 = δ) — the masks the oracle's follow mode replays.
+ * which: 0 gather-sent flag per mirror row (Alg. 2 L4), 1 master-fired flag (L15), 2 active
+ * flag (L12, L18).  uint8 per row, device pointer into the workspace.  A gather elided by
+ * elide_dead_syncs leaves its flags 0 (no mirror sends). */
+int cdfgnn_sync_flags(cdfgnn_ctx* ctx, int32_t local_part, int32_t l, int32_t dir, int32_t which,
+                      uint8_t** ptr, int64_t* rows);
+
+/* Messages received by local part `local_part` from part `src` in the most recent gather
+ * (phase 0: mirror -> master, Alg. 2 L5-L8, at the master) or scatter (phase 1: master ->
+ * mirror, L20-L22, at the mirror) phase (§5 message format).
+ *  layout 1 (slot): base = region start; slot k (k < capacity, the halo-list length) at
+ *    base + k*slot_bytes holds header {u32 stamp, f32 lo, f32 hi, u32 0} then row_bytes of
+ *    codes (or the fp32 row); slot k carries a message of that phase iff its stamp == stamp.
+ *  layout 0 (compacted): *count (device int32) messages; header k at hdr + k*hdr_bytes
+ *    ({u32 halo-list position, f32 lo, f32 hi} or {u32 position}), row k at pay + k*row_bytes;
+ *    order across blocks is not deterministic (the positions are).
+ * Device pointers into the caller's workspace (or, co-resident, the sender's region), valid
+ * until the next synchronisation; with one part per GPU the gather messages are valid only
+ * until the same synchronisation's scatter (regions are reused).  row_bytes and stamp refer
+ * to the width of that most recent phase. */
+typedef struct {
+    int32_t layout;             /* 0 compacted, 1 slot-addressed */
+    const uint8_t* base;        /* slot: region start; compacted: header array */
+    const uint8_t* pay;         /* compacted: payload rows; slot: NULL */
+    const int32_t* count;       /* compacted: device message count; slot: NULL */
+    int64_t capacity;           /* halo-list length of the (src, local part) pair */
+    int64_t hdr_bytes;          /* 16 (slot), 12 or 4 (compacted) */
+    int64_t row_bytes;          /* code / payload row bytes of the most recent phase */
+    int64_t slot_bytes;         /* slot stride (slot layout) */
+    uint32_t stamp;             /* slot layout: stamp of the most recent phase */
+    int32_t quant_bits;
+} cdfgnn_msg_view_t;
+int cdfgnn_msg_view(cdfgnn_ctx* ctx, int32_t local_part, int32_t phase, int32_t src,
+                    cdfgnn_msg_view_t* out);
 int cdfgnn_reset_caches(cdfgnn_ctx* ctx, void* stream);
 int cdfgnn_get_eps(cdfgnn_ctx* ctx, double* eps, double* mean_acc);
 int cdfgnn_set_eps(cdfgnn_ctx* ctx, double eps);

@@ -67,6 +67,14 @@ class SyncCounters:
     gather_mask: Dict[int, np.ndarray] = field(default_factory=dict)   # part -> bool[M_i]
     master_fired_mask: Dict[int, np.ndarray] = field(default_factory=dict)
     active_mask: Dict[int, np.ndarray] = field(default_factory=dict)   # part -> bool[B_i]
+    # the messages themselves (O10, §5): (src, dst) -> (pos, payload, lo, hi) where
+    # pos are the halo-list positions of the sent vertices (ascending), payload the B-bit codes
+    # q [k, F] (int64) or, without quantisation, the fp payload rows; lo, hi the per-vertex
+    # headers (None without quantisation).  gather: mirror part -> master part (position in
+    # the mirror slab of that master); scatter: master part -> mirror part (position in the
+    # halo list of that mirror part).
+    gather_msgs: Dict[tuple, tuple] = field(default_factory=dict)
+    scatter_msgs_rec: Dict[tuple, tuple] = field(default_factory=dict)
 
     @property
     def remote(self) -> int:
@@ -151,6 +159,7 @@ def sync(plan, st: SyncState, X: List[np.ndarray], eps: float, mode: SyncMode,
             if B:
                 q, qlo, qhi, deq = _q(d[rows], B, dt)
                 payload = deq
+                cnt.gather_msgs[(i, j)] = (pos, q, qlo, qhi)
                 if mode.cache:
                     if mode.snapshot_literal:
                         s[rows] = z[rows]
@@ -158,6 +167,7 @@ def sync(plan, st: SyncState, X: List[np.ndarray], eps: float, mode: SyncMode,
                         s[rows] = (s[rows] + deq).astype(dt)       # R11
             else:
                 payload = d[rows]
+                cnt.gather_msgs[(i, j)] = (pos, payload.copy(), None, None)
                 if mode.cache:
                     s[rows] = z[rows]                              # Alg. 2 L6
             msgs[(i, j)] = (pos, payload)
@@ -203,10 +213,10 @@ def sync(plan, st: SyncState, X: List[np.ndarray], eps: float, mode: SyncMode,
             delta = a[act] if mode.scatter_full else (a[act] - bold[act]).astype(dt)
             q, qlo, qhi, deq = _q(delta, B, dt)
             bnew = deq if mode.scatter_full else (bold[act] + deq).astype(dt)
-            scat[j] = (active, deq)
+            scat[j] = (active, deq, q, qlo, qhi)
         else:
             bnew = a[act].copy()
-            scat[j] = (active, bnew)
+            scat[j] = (active, bnew, bnew, None, None)
         if mode.cache:
             st.b_mas[j][act] = bnew
             out[j][:Bj] = st.b_mas[j]
@@ -224,7 +234,7 @@ def sync(plan, st: SyncState, X: List[np.ndarray], eps: float, mode: SyncMode,
         for j in range(p):
             if j == i:
                 continue
-            active, pay = scat[j]
+            active, pay, sq, slo, shi = scat[j]
             hm = plan.parts[j].halo_master[i]            # halo list (i, j) on the master side
             act_rows_j = np.flatnonzero(active)
             # payload row index for each active master of j
@@ -239,6 +249,10 @@ def sync(plan, st: SyncState, X: List[np.ndarray], eps: float, mode: SyncMode,
                 bmir[rows] = pay[sel[pos]]
             cnt.scatter_msgs += len(pos)
             cnt.bytes += len(pos) * msg_bytes(F, B)
+            k = sel[pos]
+            cnt.scatter_msgs_rec[(j, i)] = (pos, sq[k].copy(),
+                                            None if slo is None else slo[k].copy(),
+                                            None if shi is None else shi[k].copy())
         out[i][Bi:Bi + P.n_mirror] = bmir
     return out, cnt
 

@@ -71,13 +71,14 @@ class PartitionedGCN:
             if cfg.optimizer == "adam" else None
         self.epoch_no = 0
 
-    def forward(self, eps, counters):
+    def forward(self, eps, counters, follow=None):
         p = self.plan.p
         H = [[prt["X"]] for prt in self.parts]
         Z = [[] for _ in range(p)]
         for l in range(1, self.L + 1):
             Zdd = [prt["A"] @ (H[i][l - 1] @ self.W[l - 1]) for i, prt in enumerate(self.parts)]
-            Zs, c = sync(self.plan, self.fwd_state[l - 1], Zdd, eps, self.mode)
+            Zs, c = sync(self.plan, self.fwd_state[l - 1], Zdd, eps, self.mode,
+                         follow=None if follow is None else follow.get(("fwd", l)))
             counters.append(("fwd", l, c))
             for i in range(p):
                 Z[i].append(Zs[i])
@@ -85,11 +86,16 @@ class PartitionedGCN:
         return Z, H
 
     def epoch(self, follow=None):
-        """One iteration of Alg. 1.  Returns a dict of loss, acc, ε used and sync counters."""
+        """One iteration of Alg. 1.  Returns a dict of loss, acc, ε used and sync counters.
+
+        ``follow`` (trajectory follow mode): {("fwd" | "bwd", l): {"gather":
+        {i: bool[M_i]}, "master": {j: bool[B_j]}}} — the cache-test decisions of those syncs
+        are replaced by recorded ones (e.g. the GPU's), so a near-threshold flip caused by
+        rounding cannot make the two trajectories diverge; a missing key runs the test."""
         p = self.plan.p
         eps = self.eps_ctl.eps if self.cfg.cache else 0.0
         counters = []
-        Z, H = self.forward(eps, counters)
+        Z, H = self.forward(eps, counters, follow)
         # loss on masters ∩ train (P:L256), mean over the global train count (R7)
         loss = 0.0
         correct = 0
@@ -101,7 +107,8 @@ class PartitionedGCN:
             ddot.append(di)
         dW = [np.zeros_like(w) for w in self.W]
         for l in range(self.L, 0, -1):
-            delta, c = sync(self.plan, self.bwd_state[l - 1], ddot, eps, self.mode)
+            delta, c = sync(self.plan, self.bwd_state[l - 1], ddot, eps, self.mode,
+                            follow=None if follow is None else follow.get(("bwd", l)))
             counters.append(("bwd", l, c))
             nxt = []
             for i, prt in enumerate(self.parts):

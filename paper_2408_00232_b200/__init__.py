@@ -13,7 +13,7 @@ not been built — there is no fallback path.
 _API = (
     "Plan", "Ctx", "CdfgnnError", "partition", "plan_part", "plan_stats", "cfg_default",
     "get_unique_id", "workspace_size", "init", "destroy", "halo_exchange", "layer_fwd",
-    "layer_bwd", "epoch", "epoch_host", "epoch_host_next", "cache_view", "act_view", "grad_view", "sync_flags",
+    "layer_bwd", "epoch", "epoch_host", "epoch_host_next", "cache_view", "act_view", "grad_view", "sync_flags", "msg_view",
     "reset_caches", "get_eps",
     "set_eps", "spmm", "bandwidth_probe", "last_error", "version", "ld_of",
 )

@@ -68,7 +68,13 @@ class CfgC(ctypes.Structure):
                 ("eps_clamp", c_i32), ("quant_bits", c_i32), ("optimizer", c_i32), ("lr", c_f64),
                 ("beta1", c_f64), ("beta2", c_f64), ("adam_eps", c_f64), ("gemm_tf32", c_i32),
                 ("timing", c_i32), ("transport", c_i32), ("elide_dead_syncs", c_i32),
-                ("static_inputs", c_i32), ("overlap", c_i32)]
+                ("static_inputs", c_i32), ("overlap", c_i32), ("msg_layout", c_i32)]
+
+
+class MsgViewC(ctypes.Structure):
+    _fields_ = [("layout", c_i32), ("base", c_void_p), ("pay", c_void_p), ("count", c_void_p),
+                ("capacity", c_i64), ("hdr_bytes", c_i64), ("row_bytes", c_i64),
+                ("slot_bytes", c_i64), ("stamp", ctypes.c_uint32), ("quant_bits", c_i32)]
 
 
 class SyncStatsC(ctypes.Structure):
@@ -121,7 +127,8 @@ _sig("cdfgnn_epoch_host_next", c_i32, [c_void_p, P(c_void_p), P(c_void_p), P(c_v
                                        P(c_void_p), P(c_void_p), P(c_void_p), P(EpochStatsC), c_void_p])
 _sig("cdfgnn_cache_view", c_i32, [c_void_p, c_i32, c_i32, c_i32, c_i32, P(c_void_p), P(c_i64),
                                   P(c_i64)])
-_sig("cdfgnn_sync_flags", c_i32, [c_void_p, c_i32, c_i32, P(c_void_p), P(c_i64)])
+_sig("cdfgnn_sync_flags", c_i32, [c_void_p, c_i32, c_i32, c_i32, c_i32, P(c_void_p), P(c_i64)])
+_sig("cdfgnn_msg_view", c_i32, [c_void_p, c_i32, c_i32, c_i32, P(MsgViewC)])
 _sig("cdfgnn_act_view", c_i32, [c_void_p, c_i32, c_i32, P(c_void_p), P(c_i64), P(c_i64)])
 _sig("cdfgnn_grad_view", c_i32, [c_void_p, c_i32, P(c_void_p), P(c_i64), P(c_i64)])
 _sig("cdfgnn_reset_caches", c_i32, [c_void_p, c_void_p])

@@ -294,11 +294,21 @@ def grad_view(ctx: Ctx, l: int):
     return p.value, rows.value, ld.value
 
 
-def sync_flags(ctx: Ctx, local_part: int, which: int):
+def sync_flags(ctx: Ctx, local_part: int, l: int, direction: int, which: int):
+    """(device pointer, rows) of the uint8 flags of the latest sync of (l, direction):
+    which 0 gather-sent per mirror, 1 master-fired, 2 active."""
     p = ctypes.c_void_p()
     rows = L.c_i64()
-    check(_c.cdfgnn_sync_flags(ctx.handle, local_part, which, ctypes.byref(p), ctypes.byref(rows)))
+    check(_c.cdfgnn_sync_flags(ctx.handle, local_part, l, direction, which, ctypes.byref(p),
+                               ctypes.byref(rows)))
     return p.value, rows.value
+
+
+def msg_view(ctx: Ctx, local_part: int, phase: int, src: int) -> Dict:
+    """cdfgnn_msg_view as a dict (device pointers as ints)."""
+    v = L.MsgViewC()
+    check(_c.cdfgnn_msg_view(ctx.handle, local_part, phase, src, ctypes.byref(v)))
+    return {k: getattr(v, k) for k, _ in L.MsgViewC._fields_}
 
 
 def reset_caches(ctx: Ctx, stream=None):

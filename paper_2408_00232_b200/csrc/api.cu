@@ -1,11 +1,14 @@
 // libcdfgnn C ABI: context, workspace carving, halo exchange orchestration,
 // layer forward/backward and the Alg. 1 epoch.
 //
-// Transport: co-resident partitions (world == 1, k == p parts on one GPU) read
-// each other's message regions directly in device memory; one partition per GPU
-// (world == p) exchanges message counts and then payloads with grouped NCCL
-// send/recv over NVLink (§3.2 gather / scatter), and sums weight
-// gradients with ncclAllReduce (the "parameter server" of P:L221-222, reading R9).
+// Transport (§3.2 gather / scatter): co-resident partitions (world == 1, k == p
+// parts on one GPU) and the NVLink push transport (world == p, one part per GPU, peers'
+// workspaces mapped with CUDA IPC) use slot-addressed message regions — a message lives in
+// the slot of its vertex's halo-list position, stamped with the phase's sequence number, and
+// the sending kernel stores it straight into the receiver's region (kernels_halo.cu).  The
+// NCCL transport (transport = 1) packs compacted per-peer buffers and exchanges counts and
+// payloads with grouped send/recv.  Weight gradients are summed with ncclAllReduce (the
+// "parameter server" of P:L221-222, reading R9).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -17,6 +20,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.h"
@@ -105,10 +109,13 @@ struct LocalPart {
     RegionTab *gsend_d = nullptr, *grecv_d = nullptr, *ssend_d = nullptr, *srecv_d = nullptr;
     RegionTab gsend_h{}, grecv_h{}, ssend_h{}, srecv_h{};
     PutTab *putG_d = nullptr, *putS_d = nullptr;   // NVLink push of gather / scatter messages
+    SlotTab gdst{}, gsrc{}, sdst{}, ssrc{};   // slot layout: gather / scatter destination and source regions
+    int32_t* hpos = nullptr;           // [B*p] slot of master row r in the halo list shared with part s
+    std::vector<int32_t> hpos_h;
     uint64_t* bar = nullptr;           // [p] NVLink barrier arrival slots (written by the peers)
     int32_t* cnt = nullptr;           // [4p]: gsend | grecv | ssend | srecv
     int32_t* cnt_h = nullptr;         // pinned
-    uint8_t *gflag = nullptr, *fired = nullptr, *active = nullptr;
+    uint8_t *gflag = nullptr, *fired = nullptr, *active = nullptr;   // [L][2][M] / [L][2][B] per sync
     int32_t *idxmap = nullptr, *mmap = nullptr;
     uint8_t* stage_codes = nullptr;
     float *stage_lohi = nullptr, *stage_a = nullptr;
@@ -132,7 +139,12 @@ struct cdfgnn_ctx {
     int32_t p = 0, k = 0, rank = 0, world = 1, device = 0;
     std::vector<LocalPart> parts;
     ncclComm_t comm = nullptr;
-    int64_t Fmax = 0, ldmax = 0, hdr_bytes = 4, wtotal = 0;
+    int64_t Fmax = 0, ldmax = 0, hdr_bytes = 4, wtotal = 0, rowb_max = 0;
+    bool slot = false;                 // slot-addressed message layout (co-resident, NVLink push)
+    uint32_t seq = 0;                  // message stamps (slot layout), identical on every rank
+    uint32_t stamp[CDFGNN_MAX_LAYERS][2][2] = {};   // (l, dir) -> gather / scatter stamp of the sync in flight
+    uint32_t last_stamp[2] = {0, 0};   // most recent gather / scatter stamp (cdfgnn_msg_view)
+    int64_t last_ld[2] = {0, 0};
     int64_t woff[CDFGNN_MAX_LAYERS + 1] = {};
     int64_t splitk_cap = 0;
     float *dW = nullptr, *adam_m = nullptr, *adam_v = nullptr, *splitk = nullptr;
@@ -176,6 +188,13 @@ struct cdfgnn_ctx {
     // world > 1: input rows of mirrors are filled from their masters over NCCL (own communicator,
     // issued only on the copy stream cs), so each vertex's features cross PCIe once
     ncclComm_t comm_in = nullptr;
+    // §8 f2: each layer's ∇W allreduce runs on its own communicator and stream as soon as the
+    // layer's ∇W is complete, under the lower layers' backward (reading R8); joined before the
+    // optimizer
+    ncclComm_t comm_grad = nullptr;
+    cudaStream_t s3 = nullptr;
+    cudaEvent_t evG = nullptr, evJ = nullptr;
+    bool dw_pending = false;
 };
 
 namespace {
@@ -299,7 +318,9 @@ int prepare(cdfgnn_ctx* c, const cdfgnn_plan* plan, const int32_t* parts, int32_
     c->p = cdfgnn_plan_num_parts(plan);
     c->k = k;
     if (cfg->L < 1 || cfg->L > CDFGNN_MAX_LAYERS) CDF_FAIL(CDFGNN_EUSAGE, "L must be in [1, %d]", CDFGNN_MAX_LAYERS);
-    if (cfg->quant_bits != 0 && cfg->quant_bits != 8) CDF_FAIL(CDFGNN_EUSAGE, "quant_bits must be 0 or 8");
+    if (cfg->quant_bits != 0 && cfg->quant_bits != 4 && cfg->quant_bits != 8 && cfg->quant_bits != 16)
+        CDF_FAIL(CDFGNN_EUSAGE, "quant_bits must be 0, 4, 8 or 16");
+    if (cfg->msg_layout < 0 || cfg->msg_layout > 2) CDF_FAIL(CDFGNN_EUSAGE, "msg_layout must be 0, 1 or 2");
     for (int l = 0; l <= cfg->L; ++l)
         if (cfg->dims[l] < 1) CDF_FAIL(CDFGNN_EUSAGE, "dims[%d] must be >= 1", l);
     for (int l = 1; l <= cfg->L; ++l)
@@ -310,6 +331,7 @@ int prepare(cdfgnn_ctx* c, const cdfgnn_plan* plan, const int32_t* parts, int32_
     for (int l = 1; l <= cfg->L; ++l) c->Fmax = std::max<int64_t>(c->Fmax, cfg->dims[l]);
     c->ldmax = ld_of(c->Fmax);
     c->hdr_bytes = cfg->quant_bits ? 12 : 4;
+    c->rowb_max = code_row_bytes(cfg->quant_bits, c->ldmax);
     c->wtotal = 0;
     for (int l = 1; l <= cfg->L; ++l) {
         c->woff[l - 1] = c->wtotal;
@@ -348,6 +370,11 @@ int prepare(cdfgnn_ctx* c, const cdfgnn_plan* plan, const int32_t* parts, int32_
             P.capA[j] = P.moff[j + 1] - P.moff[j];
             P.capB[j] = P.hoff[j + 1] - P.hoff[j];
         }
+        // slot of each boundary master row in the halo list shared with each peer (static)
+        P.hpos_h.assign((size_t)P.B * c->p, -1);
+        for (int q = 0; q < c->p; ++q)
+            for (int64_t k = P.hoff[q]; k < P.hoff[q + 1]; ++k)
+                P.hpos_h[(size_t)v.halo_local[k] * c->p + q] = (int32_t)(k - P.hoff[q]);
         // wide rows: LPT over whole rows (chunks cost L2 bandwidth there, profiles/r1);
         // narrow rows: hub rows split into chunks (their latency chains dominated)
         build_spmm_items(P, P.sp[0], spmm_chunk(true, P.nnz), spmm_default_phases(), spmm_phase_min_degree());
@@ -358,9 +385,10 @@ int prepare(cdfgnn_ctx* c, const cdfgnn_plan* plan, const int32_t* parts, int32_
     return CDFGNN_OK;
 }
 
+// a region holds either layout: compacted (header array, then rows) or slot-addressed
 int64_t region_bytes(const cdfgnn_ctx* c, int64_t cap) {
-    const int64_t rowb = c->cfg.quant_bits ? c->ldmax : 4 * c->ldmax;   // code rows: ld bytes
-    return align_up(cap * c->hdr_bytes, 256) + cap * rowb;
+    const int64_t packed = align_up(cap * c->hdr_bytes, 256) + cap * c->rowb_max;
+    return std::max(packed, cap * slot_stride(c->cfg.quant_bits, c->ldmax));
 }
 
 void carve(cdfgnn_ctx* c, Bump& b) {
@@ -392,12 +420,13 @@ void carve(cdfgnn_ctx* c, Bump& b) {
         P.putS_d = b.take<PutTab>(1);
         P.cnt = b.take<int32_t>(4 * p);
         P.bar = b.take<uint64_t>(p);
-        P.gflag = b.take<uint8_t>(P.M);
-        P.fired = b.take<uint8_t>(P.B);
-        P.active = b.take<uint8_t>(P.B);
+        P.gflag = b.take<uint8_t>(2 * L * P.M);
+        P.fired = b.take<uint8_t>(2 * L * P.B);
+        P.active = b.take<uint8_t>(2 * L * P.B);
+        P.hpos = b.take<int32_t>((int64_t)p * P.B);
         P.idxmap = b.take<int32_t>((int64_t)p * P.B);
         P.mmap = b.take<int32_t>(P.M);
-        P.stage_codes = b.take<uint8_t>(P.B * c->ldmax);
+        P.stage_codes = b.take<uint8_t>(P.B * c->rowb_max);
         P.stage_lohi = b.take<float>(2 * P.B);
         P.stage_a = b.take<float>(P.B * c->ldmax);
         for (int l = 1; l <= L; ++l) {
@@ -492,6 +521,11 @@ void build_tables(cdfgnn_ctx* c) {
             if (c->world == 1) {
                 // co-resident partitions: read the sender's region in place
                 LocalPart& Q = c->parts[s];
+                // slot layout: a sender stores into its own region, the receiver reads it there
+                P.gdst.base[s] = s == me ? nullptr : P.regA[s];
+                P.gsrc.base[s] = s == me ? nullptr : Q.regA[me];
+                P.sdst.base[s] = s == me ? nullptr : P.regB[s];
+                P.ssrc.base[s] = s == me ? nullptr : Q.regB[me];
                 P.grecv_h.hdr[s] = Q.gsend_h.hdr[me];
                 P.grecv_h.pay[s] = Q.gsend_h.pay[me];
                 P.grecv_h.cnt[s] = Q.gsend_h.cnt[me];
@@ -505,6 +539,10 @@ void build_tables(cdfgnn_ctx* c) {
                 P.srecv_h.hdr[s] = P.regA[s];
                 P.srecv_h.pay[s] = P.gsend_h.pay[s];
                 P.srecv_h.cnt[s] = P.cnt + 3 * p + s;
+                // slot layout (push): receive in the own regions; destinations are mapped by
+                // setup_push (peers' regB[me] for the gather, regA[me] for the scatter)
+                P.gsrc.base[s] = s == me ? nullptr : P.regB[s];
+                P.ssrc.base[s] = s == me ? nullptr : P.regA[s];
             }
         }
         HaloDev& h = P.halo;
@@ -517,6 +555,7 @@ void build_tables(cdfgnn_ctx* c) {
         h.idxmap = P.idxmap; h.mmap = P.mmap;
         h.stage_codes = P.stage_codes; h.stage_lohi = P.stage_lohi; h.stage_a = P.stage_a;
         h.err = c->scal_d + 1;
+        h.hpos = P.hpos;
     }
 }
 
@@ -537,6 +576,33 @@ int check_launch(const char* what) {
     return CDFGNN_OK;
 }
 
+// Host wait on `s` that notices a failed or dead peer: while the stream is busy, poll the
+// communicators' asynchronous error state; an NCCL error aborts the communicators (so
+// their kernels return) and maps to ENCCL instead of hanging in cudaStreamSynchronize.
+int wait_stream(cdfgnn_ctx* c, cudaStream_t s) {
+    if (!c->comm) {
+        CUDA_TRY(cudaStreamSynchronize(s));
+        return CDFGNN_OK;
+    }
+    for (unsigned spin = 0;; ++spin) {
+        const cudaError_t e = cudaStreamQuery(s);
+        if (e == cudaSuccess) return CDFGNN_OK;
+        if (e != cudaErrorNotReady) CDF_FAIL(CDFGNN_ECUDA, "stream: %s", cudaGetErrorString(e));
+        for (ncclComm_t cm : {c->comm, c->comm_in, c->comm_grad}) {
+            if (!cm) continue;
+            ncclResult_t ae = ncclSuccess;
+            if (ncclCommGetAsyncError(cm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress) {
+                ncclCommAbort(c->comm);
+                if (c->comm_in) ncclCommAbort(c->comm_in);
+                if (c->comm_grad) ncclCommAbort(c->comm_grad);
+                c->comm = c->comm_in = c->comm_grad = nullptr;
+                CDF_FAIL(CDFGNN_ENCCL, "NCCL asynchronous error: %s", ncclGetErrorString(ae));
+            }
+        }
+        if (spin > 64) std::this_thread::yield();
+    }
+}
+
 // NCCL count + payload exchange for one phase (world > 1, k == 1)
 int nccl_phase(cdfgnn_ctx* c, LocalPart& P, bool gather, int64_t rowb, cudaStream_t s,
                int64_t* wire) {
@@ -551,7 +617,7 @@ int nccl_phase(cdfgnn_ctx* c, LocalPart& P, bool gather, int64_t rowb, cudaStrea
     }
     NCCL_TRY(ncclGroupEnd());
     CUDA_TRY(cudaMemcpyAsync(P.cnt_h, P.cnt, sizeof(int32_t) * 4 * p, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
+    CDF_TRY(wait_stream(c, s));
     const int32_t* hs = P.cnt_h + (gather ? 0 : 2 * p);
     const int32_t* hr = P.cnt_h + (gather ? p : 3 * p);
     const RegionTab& st = gather ? P.gsend_h : P.ssend_h;
@@ -671,6 +737,9 @@ int setup_push(cdfgnn_ctx* c, cudaStream_t s) {
         ps.dst_hdr[r] = pws + all[r].regA_off[me];
         ps.dst_pay[r] = ps.dst_hdr[r] + align_up(P.capB[r] * c->hdr_bytes, 256);
         ps.dst_cnt[r] = pcnt + 3 * p + me;
+        // slot layout: the kernels store straight into the peer's regions
+        P.gdst.base[r] = pg.dst_hdr[r];
+        P.sdst.base[r] = ps.dst_hdr[r];
     }
     CUDA_TRY(cudaMemcpyAsync(P.putG_d, &pg, sizeof(PutTab), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(P.putS_d, &ps, sizeof(PutTab), cudaMemcpyHostToDevice, s));
@@ -690,8 +759,9 @@ int setup_push(cdfgnn_ctx* c, cudaStream_t s) {
 }
 
 void sync_args(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float eps, bool skip_gather,
-               std::vector<SyncArgs>& args) {
+               std::vector<SyncArgs>& args, bool skip_scatter = false) {
     const int F = (int)sync_width(c, l);
+    const int bits = c->cfg.quant_bits;
     args.assign(c->k, SyncArgs{});
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
@@ -701,7 +771,32 @@ void sync_args(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float
         a.c = P.cache[l - 1][dir];
         a.stats = c->stats_d + ((l - 1) * 2 + dir) * 4;
         a.no_msgs = skip_gather ? 1 : 0;
+        a.no_scatter = skip_scatter ? 1 : 0;
+        a.rowb = code_row_bytes(bits, ld);
+        a.stride = slot_stride(bits, ld);
+        a.gstamp = c->stamp[l - 1][dir][0];
+        a.sstamp = c->stamp[l - 1][dir][1];
     }
+}
+
+// the part's halo descriptor with the send / fired / active flags of sync (l, dir)
+HaloDev halo_for(const cdfgnn_ctx* c, const LocalPart& P, int l, int dir) {
+    HaloDev h = P.halo;
+    const int64_t k = (int64_t)(l - 1) * 2 + dir;
+    h.gflag = P.gflag + k * P.M;
+    h.fired = P.fired + k * P.B;
+    h.active = P.active + k * P.B;
+    return h;
+}
+
+// slot layout: fresh stamps for the two phases of sync (l, dir) — every rank runs the same
+// sequence of syncs, so the stamps agree across ranks
+void new_stamps(cdfgnn_ctx* c, int l, int dir, int64_t ld) {
+    c->stamp[l - 1][dir][0] = ++c->seq;
+    c->stamp[l - 1][dir][1] = ++c->seq;
+    c->last_stamp[0] = c->stamp[l - 1][dir][0];
+    c->last_stamp[1] = c->stamp[l - 1][dir][1];
+    c->last_ld[0] = c->last_ld[1] = ld;
 }
 
 // Gather phase of one synchronisation (Alg. 2 L3-L9): mirrors test, quantise, pack, and the
@@ -713,12 +808,23 @@ int halo_gather(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, floa
     if (ld != ld_of(F)) CDF_FAIL(CDFGNN_EUSAGE, "ld %lld must equal roundup(F=%d, 4)", (long long)ld, F);
     std::vector<SyncArgs> args;
     sync_args(c, l, dir, X, ld, eps, false, args);
-    const int64_t rowb = c->cfg.quant_bits ? ld : 4 * ld;   // code rows padded to ld bytes
+    const int64_t rowb = code_row_bytes(c->cfg.quant_bits, ld);
+    if (c->slot) {
+        // senders store straight into the masters' slots (own region co-resident, peer GPU push)
+        for (int t = 0; t < c->k; ++t) {
+            LocalPart& P = c->parts[t];
+            c->launches += launch_gather_slot(halo_for(c, P, l, dir), args[t], P.gdst, s);
+        }
+        CDF_TRY(check_launch("gather_slot"));
+        if (!(c->s2 && s == c->s2)) mark(c, PH_SYNC, s, SS_GXFER);
+        if (c->transport == 2) CDF_TRY(push_barrier(c, s));
+        return CDFGNN_OK;
+    }
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
         const int nt = gather_tiles_host(P.moff.data(), p, ld);
         CUDA_TRY(cudaMemsetAsync(P.cnt, 0, sizeof(int32_t) * p, s));       // range reservations
-        c->launches += launch_gather_pack_n(P.halo, args[t], nt, s);
+        c->launches += launch_gather_pack_n(halo_for(c, P, l, dir), args[t], nt, s);
     }
     CDF_TRY(check_launch("gather_pack"));
     if (!(c->s2 && s == c->s2)) mark(c, PH_SYNC, s, SS_GXFER);   // no marks on the side stream
@@ -737,11 +843,28 @@ int halo_gather(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, floa
 int halo_finish(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float eps,
                 cudaStream_t s, int64_t* wire, bool skip_gather, bool skip_scatter) {
     const int p = c->p;
-    const int F = (int)sync_width(c, l);
     std::vector<SyncArgs> args;
-    sync_args(c, l, dir, X, ld, eps, skip_gather, args);
-    const int64_t rowb = c->cfg.quant_bits ? ld : 4 * ld;   // code rows padded to ld bytes
+    sync_args(c, l, dir, X, ld, eps, skip_gather, args, skip_scatter);
+    const int64_t rowb = code_row_bytes(c->cfg.quant_bits, ld);
     mark(c, PH_SYNC, s, SS_MASTER);
+    if (c->slot) {
+        // masters apply their slots in ascending source order, their own Δ, and store the
+        // scatter messages straight into the mirrors' slots (one kernel, L10-L22)
+        for (int t = 0; t < c->k; ++t) {
+            LocalPart& P = c->parts[t];
+            c->launches += launch_master_slot(halo_for(c, P, l, dir), args[t], P.gsrc, P.sdst, s);
+        }
+        CDF_TRY(check_launch("master_slot"));
+        if (skip_scatter) return CDFGNN_OK;
+        mark(c, PH_SYNC, s, SS_SXFER);
+        if (c->transport == 2) CDF_TRY(push_barrier(c, s));
+        mark(c, PH_SYNC, s, SS_MIRROR);
+        for (int t = 0; t < c->k; ++t) {
+            LocalPart& P = c->parts[t];
+            c->launches += launch_mirror_slot(halo_for(c, P, l, dir), args[t], P.ssrc, s);
+        }
+        return check_launch("mirror_slot");
+    }
     // ---- masters: apply in ascending source order, own test, stage scatter (L10-L19)
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
@@ -750,7 +873,7 @@ int halo_finish(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, floa
             CUDA_TRY(cudaMemsetAsync(P.idxmap, 0xFF, sizeof(int32_t) * p * P.B, s));
             c->launches += launch_map(P.halo, P.grecv_h, 0, *std::max_element(P.capB.begin(), P.capB.end()), s);
         }
-        c->launches += launch_master(P.halo, args[t], P.grecv_h, s);
+        c->launches += launch_master(halo_for(c, P, l, dir), args[t], P.grecv_h, s);
     }
     CDF_TRY(check_launch("master"));
     if (skip_scatter) return CDFGNN_OK;
@@ -760,7 +883,7 @@ int halo_finish(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, floa
         LocalPart& P = c->parts[t];
         const int nt = scatter_tiles_host(P.hoff.data(), p);
         CUDA_TRY(cudaMemsetAsync(P.cnt + 2 * p, 0, sizeof(int32_t) * p, s));
-        c->launches += launch_scatter_pack_n(P.halo, args[t], nt, s);
+        c->launches += launch_scatter_pack_n(halo_for(c, P, l, dir), args[t], nt, s);
     }
     CDF_TRY(check_launch("scatter_pack"));
     mark(c, PH_SYNC, s, SS_SXFER);
@@ -778,7 +901,7 @@ int halo_finish(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, floa
         if (P.M == 0) continue;
         CUDA_TRY(cudaMemsetAsync(P.mmap, 0xFF, sizeof(int32_t) * P.M, s));
         c->launches += launch_map(P.halo, P.srecv_h, 1, *std::max_element(P.capA.begin(), P.capA.end()), s);
-        c->launches += launch_mirror_apply(P.halo, args[t], P.srecv_h, s);
+        c->launches += launch_mirror_apply(halo_for(c, P, l, dir), args[t], P.srecv_h, s);
     }
     CDF_TRY(check_launch("mirror_apply"));
     return CDFGNN_OK;
@@ -791,6 +914,7 @@ int halo_impl(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float 
               cudaStream_t s, int64_t* wire, bool skip_gather = false, bool skip_scatter = false) {
     const int F = (int)sync_width(c, l);
     if (ld != ld_of(F)) CDF_FAIL(CDFGNN_EUSAGE, "ld %lld must equal roundup(F=%d, 4)", (long long)ld, F);
+    new_stamps(c, l, dir, ld);
     mark(c, PH_SYNC, s, SS_GPACK);
     if (!skip_gather) CDF_TRY(halo_gather(c, l, dir, X, ld, eps, s, wire));
     else mark(c, PH_SYNC, s, SS_GXFER);
@@ -808,6 +932,7 @@ int launch_gather_async(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t 
     cudaStream_t gs = serial ? s : c->s2;
     CUDA_TRY(cudaEventRecord(c->evA, s));
     CUDA_TRY(cudaStreamWaitEvent(gs, c->evA, 0));
+    new_stamps(c, l, dir, ld);
     CDF_TRY(halo_gather(c, l, dir, X, ld, eps, gs, wire));
     CUDA_TRY(cudaEventRecord(c->evB, gs));
     c->pend[l - 1][dir] = true;
@@ -833,11 +958,15 @@ void fill_sync_stats(const cdfgnn_ctx* c, int l, int dir, const unsigned long lo
     int64_t M = 0;
     for (const LocalPart& P : c->parts) M += P.M;
     st->baseline = 2 * M;
-    const int64_t mb = c->cfg.quant_bits ? F + 12 : 4 * F + 4;
+    // O9 / R25: B·F bits of codes + 2·32 bits (lo, hi) + a 32-bit position per quantised
+    // message (F + 12 bytes at B = 8), 4F + 4 bytes per fp32 message
+    const int B = c->cfg.quant_bits;
+    const int64_t mb = B ? (B * F + 7) / 8 + 12 : 4 * F + 4;
     st->bytes_alg = (h[0] + h[3]) * mb;
     st->bytes_wire = wire;
     if (c->transport == 2)      // NVLink push: every message is stored into a peer GPU
-        st->bytes_wire = (int64_t)(h[0] + h[3]) * (c->hdr_bytes + (c->cfg.quant_bits ? ld_of(F) : 4 * ld_of(F)));
+        st->bytes_wire = (int64_t)(h[0] + h[3]) *
+                         (c->slot ? 16 + code_row_bytes(B, ld_of(F)) : c->hdr_bytes + code_row_bytes(B, ld_of(F)));
     (void)dir;
 }
 
@@ -845,7 +974,7 @@ int read_stats_now(cdfgnn_ctx* c, int l, int dir, int64_t wire, cudaStream_t s,
                    cdfgnn_sync_stats* st) {
     unsigned long long* slot = c->stats_d + ((l - 1) * 2 + dir) * 4;
     CUDA_TRY(cudaMemcpyAsync(c->stats_h, slot, sizeof(long long) * 4, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
+    CDF_TRY(wait_stream(c, s));
     fill_sync_stats(c, l, dir, c->stats_h, wire, st);
     return CDFGNN_OK;
 }
@@ -881,12 +1010,18 @@ int ensure_ax(cdfgnn_ctx* c, LocalPart& P, const float* X, int64_t ld_in, cudaSt
     const int64_t F0 = c->cfg.dims[0];
     if (ld_in != ld_of(F0)) CDF_FAIL(CDFGNN_EUSAGE, "hoisted input aggregation needs ld(X) = %lld",
                                      (long long)ld_of(F0));
-    const SpmmPlan& S = spmm_plan(P, ld_in);
-    if (S.nslots && ld_in > S.pstride) CDF_FAIL(CDFGNN_EUSAGE, "split SpMM rows cannot hold ld %lld",
-                                                (long long)ld_in);
+    // the SpMM kernels cover <= 1024 columns per launch: wider inputs (C1's 1433 features)
+    // are aggregated in 1024-column slices of the same rows
+    const int64_t w0 = std::min<int64_t>(ld_in, 1024);
+    const SpmmPlan& S = spmm_plan(P, w0);
+    if (S.nslots && w0 > S.pstride) CDF_FAIL(CDFGNN_EUSAGE, "split SpMM rows cannot hold width %lld",
+                                             (long long)w0);
     mark(c, PH_OTHER, s);
-    launch_spmm(P.rowptr, P.colidx, P.val, S.n_items, spmm_items(P, 0, ld_in), X, P.ax, ld_in, s);
-    c->launches++;
+    for (int64_t c0 = 0; c0 < ld_in; c0 += 1024) {
+        const int64_t w = std::min<int64_t>(ld_in - c0, 1024);
+        launch_spmm(P.rowptr, P.colidx, P.val, S.n_items, spmm_items(P, 0, w0), X + c0, P.ax + c0, ld_in, s, w);
+        c->launches++;
+    }
     CDF_TRY(check_launch("spmm (input aggregation)"));
     if (P.xT && !wgrad_mn()) {
         c->launches += launch_transpose(P.ax, P.n, F0, ld_in, P.xT, ld_of(P.n), s);
@@ -1034,6 +1169,14 @@ int bwd_impl(cdfgnn_ctx* c, int l, float* const* dZ, int64_t ld, const float* co
             c->launches += 2;
         }
         CDF_TRY(check_launch("gemm wgrad"));
+        if (t == c->k - 1 && c->in_epoch && c->comm_grad) {
+            // ∇W^(l-1) is final on this rank: sum it over the ranks on the side stream while the
+            // remaining backward (δ̈^(l-1), the layer l-1 sync, SpMM and GEMMs) runs on s
+            CUDA_TRY(cudaEventRecord(c->evG, s));
+            CUDA_TRY(cudaStreamWaitEvent(c->s3, c->evG, 0));
+            NCCL_TRY(ncclAllReduce(dW, dW, (size_t)(Fi * Fo), ncclFloat32, ncclSum, c->comm_grad, c->s3));
+            c->dw_pending = true;
+        }
         if (dZ_prev) {
             if (ov) {
                 CDF_TRY(bwd_data_rows(t, 0, P.B));
@@ -1077,6 +1220,7 @@ extern "C" int cdfgnn_cfg_default(cdfgnn_cfg* cfg) {
     cfg->elide_dead_syncs = 1;
     cfg->static_inputs = 0;
     cfg->overlap = 0;
+    cfg->msg_layout = 0;
     return CDFGNN_OK;
 }
 
@@ -1162,6 +1306,15 @@ extern "C" int cdfgnn_init(const cdfgnn_plan* plan, const int32_t* parts, int32_
         std::memcpy(&id, nccl_uid, sizeof(id));
         NCCL_TRY(ncclCommInitRank(&c->comm, world, id, rank));
         NCCL_TRY(ncclCommSplit(c->comm, 0, rank, &c->comm_in, nullptr));
+        const char* dwo = getenv("CDFGNN_DW_OVERLAP");      // 0: one grouped allreduce after the backward
+        if (!(dwo && atoi(dwo) == 0)) {
+            NCCL_TRY(ncclCommSplit(c->comm, 0, rank, &c->comm_grad, nullptr));
+            int plo = 0, phi = 0;
+            CUDA_TRY(cudaDeviceGetStreamPriorityRange(&plo, &phi));
+            CUDA_TRY(cudaStreamCreateWithPriority(&c->s3, cudaStreamNonBlocking, phi));
+            CUDA_TRY(cudaEventCreateWithFlags(&c->evG, cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&c->evJ, cudaEventDisableTiming));
+        }
         {
             // establish the input-distribution peer connections now (NCCL connects p2p lazily,
             // which would otherwise land inside the first pipelined epochs)
@@ -1198,6 +1351,18 @@ extern "C" int cdfgnn_init(const cdfgnn_plan* plan, const int32_t* parts, int32_
             }
         }
     }
+    // message layout: slot-addressed for co-resident parts and the NVLink push transport
+    // (msg_layout 0 = auto, 2 = slot), compacted for NCCL send/recv (and msg_layout 1)
+    if (cfg->msg_layout == 2 && c->transport == 1)
+        CDF_FAIL(CDFGNN_EUSAGE, "msg_layout = 2 (slot) needs co-resident parts or the NVLink push transport");
+    c->slot = cfg->msg_layout == 2 || (cfg->msg_layout == 0 && c->transport != 1);
+    for (LocalPart& P : c->parts) {
+        if (P.B > 0)
+            CUDA_TRY(cudaMemcpyAsync(P.hpos, P.hpos_h.data(), sizeof(int32_t) * P.hpos_h.size(),
+                                     cudaMemcpyHostToDevice, s));
+        P.halo.remote = (c->slot && c->transport == 2) ? 1 : 0;   // kernels store into peer GPUs
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
     if (cfg->overlap && c->p > 1) {
         int lo = 0, hi = 0;
         CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1216,6 +1381,13 @@ extern "C" int cdfgnn_destroy(cdfgnn_ctx* c) {
     if (!c->peer_maps.empty()) cudaDeviceSynchronize();
     for (void* m : c->peer_maps) cudaIpcCloseMemHandle(m);
     if (c->comm_in) ncclCommDestroy(c->comm_in);
+    if (c->s3) {
+        cudaStreamSynchronize(c->s3);
+        cudaStreamDestroy(c->s3);
+    }
+    if (c->evG) cudaEventDestroy(c->evG);
+    if (c->evJ) cudaEventDestroy(c->evJ);
+    if (c->comm_grad) ncclCommDestroy(c->comm_grad);
     if (c->comm) ncclCommDestroy(c->comm);
     for (LocalPart& P : c->parts)
         if (P.cnt_h) cudaFreeHost(P.cnt_h);
@@ -1293,6 +1465,11 @@ static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const
     c->launches = 0;
     c->ev_used = 0;
     std::memset(c->pend, 0, sizeof(c->pend));
+    if (c->dw_pending) {               // an earlier epoch failed between a ∇W allreduce and the join
+        CUDA_TRY(cudaEventRecord(c->evJ, c->s3));
+        CUDA_TRY(cudaStreamWaitEvent(s, c->evJ, 0));
+        c->dw_pending = false;
+    }
     int64_t wire[CDFGNN_MAX_LAYERS][2] = {};
     CUDA_TRY(cudaMemsetAsync(c->stats_d, 0, sizeof(long long) * CDFGNN_MAX_LAYERS * 2 * 4, s));
     CUDA_TRY(cudaMemsetAsync(c->scal_d, 0, sizeof(int32_t) * 8, s));
@@ -1308,7 +1485,7 @@ static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const
             NCCL_TRY(ncclAllReduce(c->scal_d + 2, c->scal_d + 2, 1, ncclInt32, ncclSum, c->comm, s));
         int32_t* hs = reinterpret_cast<int32_t*>(c->host_scratch);
         CUDA_TRY(cudaMemcpyAsync(hs, c->scal_d + 2, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
+        CDF_TRY(wait_stream(c, s));
         c->ntrain = hs[0];
         if (c->ntrain <= 0) CDF_FAIL(CDFGNN_EDATA, "no training vertices");
     }
@@ -1356,11 +1533,20 @@ static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const
     }
     // ---- parameter aggregation + update (Alg. 1 L12-L13)
     mark(c, PH_OTHER, s);
+    if (c->dw_pending) {
+        CUDA_TRY(cudaEventRecord(c->evJ, c->s3));     // join the per-layer ∇W allreduces
+        CUDA_TRY(cudaStreamWaitEvent(s, c->evJ, 0));
+        c->dw_pending = false;
+    }
     if (c->world > 1) {
         NCCL_TRY(ncclGroupStart());
-        NCCL_TRY(ncclAllReduce(c->dW, c->dW, (size_t)c->wtotal, ncclFloat32, ncclSum, c->comm, s));
+        if (!c->comm_grad)
+            NCCL_TRY(ncclAllReduce(c->dW, c->dW, (size_t)c->wtotal, ncclFloat32, ncclSum, c->comm, s));
         NCCL_TRY(ncclAllReduce(c->loss_d, c->loss_d, 1, ncclFloat64, ncclSum, c->comm, s));
         NCCL_TRY(ncclAllReduce(c->scal_d, c->scal_d, 1, ncclInt32, ncclSum, c->comm, s));
+        // the error word (label out of range, halo overflow, barrier timeout) is max-reduced so
+        // every rank skips the update below and reports the error (no rank runs on alone)
+        NCCL_TRY(ncclAllReduce(c->scal_d + 1, c->scal_d + 1, 1, ncclInt32, ncclMax, c->comm, s));
         NCCL_TRY(ncclGroupEnd());
     }
     c->step_t++;
@@ -1370,7 +1556,7 @@ static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const
         const int64_t off = c->woff[l - 1], cnt = c->woff[l] - off;
         launch_optimizer(c->cfg.optimizer, W[l - 1], c->dW + off, c->adam_m + off, c->adam_v + off,
                          cnt, (float)c->cfg.lr, (float)c->cfg.beta1, (float)c->cfg.beta2,
-                         (float)c->cfg.adam_eps, (float)bc1, (float)bc2, s);
+                         (float)c->cfg.adam_eps, (float)bc1, (float)bc2, c->scal_d + 1, s);
         c->launches++;
     }
     CDF_TRY(check_launch("optimizer"));
@@ -1381,9 +1567,12 @@ static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const
     int32_t* hi = reinterpret_cast<int32_t*>(hd + k);
     CUDA_TRY(cudaMemcpyAsync(hi, c->scal_d, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(c->stats_h, c->stats_d, sizeof(long long) * L * 2 * 4, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    if (hi[1] == 3) CDF_FAIL(CDFGNN_EDATA, "label out of range");
-    if (hi[1] != 0) CDF_FAIL(CDFGNN_EPROTO, "halo protocol violation (code %d)", hi[1]);
+    CDF_TRY(wait_stream(c, s));
+    if (hi[1] != 0) {
+        c->step_t--;                   // the optimizer skipped this epoch's update (W unchanged)
+        if (hi[1] == 3) CDF_FAIL(CDFGNN_EDATA, "label out of range");
+        CDF_FAIL(CDFGNN_EPROTO, "halo protocol violation (code %d)", hi[1]);
+    }
     double loss = 0.0;
     for (int t = 0; t < k; ++t) loss += hd[t];
     loss /= (double)c->ntrain;
@@ -1478,6 +1667,10 @@ int copy_inputs(cdfgnn_ctx* c, int slot, const float* const* X_host, const int32
         LocalPart& P = c->parts[t];
         float* X; int32_t* lab; uint8_t* msk;
         stage_slot(P, slot, &X, &lab, &msk);
+        // new contents in a library-owned staging buffer: the per-X-buffer caches of
+        // static_inputs (Â_i X_i, Xᵀ) keyed on its pointer are stale
+        if (P.ax_src == X) P.ax_src = nullptr;
+        if (P.xT_src == X) P.xT_src = nullptr;
         if (c->comm_in) {
             // owned rows only (boundary masters [0, B), interior [B + M, n)); the M mirror rows
             // are replicas of other parts' masters and arrive from them below
@@ -1587,6 +1780,8 @@ extern "C" int cdfgnn_epoch_host(cdfgnn_ctx* c, const float* const* X_host,
     std::vector<const uint8_t*> msk(c->k);
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
+        if (P.ax_src == P.X_stage) P.ax_src = nullptr;     // staging rewritten: static-input caches stale
+        if (P.xT_src == P.X_stage) P.xT_src = nullptr;
         CUDA_TRY(cudaMemcpyAsync(P.X_stage, X_host[t], sizeof(float) * P.n * ld0, cudaMemcpyHostToDevice, s));
         CUDA_TRY(cudaMemcpyAsync(P.lab_stage, labels_host[t], sizeof(int32_t) * P.n, cudaMemcpyHostToDevice, s));
         CUDA_TRY(cudaMemcpyAsync(P.mask_stage, train_mask_host[t], P.n, cudaMemcpyHostToDevice, s));
@@ -1637,15 +1832,49 @@ extern "C" int cdfgnn_grad_view(cdfgnn_ctx* c, int32_t l, float** ptr, int64_t* 
     return CDFGNN_OK;
 }
 
-extern "C" int cdfgnn_sync_flags(cdfgnn_ctx* c, int32_t lp, int32_t which, uint8_t** ptr, int64_t* rows) {
+extern "C" int cdfgnn_sync_flags(cdfgnn_ctx* c, int32_t lp, int32_t l, int32_t dir, int32_t which,
+                                 uint8_t** ptr, int64_t* rows) {
     if (!c || !ptr || !rows) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
     if (lp < 0 || lp >= c->k) CDF_FAIL(CDFGNN_EUSAGE, "bad part");
+    if (l < 1 || l > c->cfg.L || dir < 0 || dir > 1) CDF_FAIL(CDFGNN_EUSAGE, "bad layer/dir");
     const LocalPart& P = c->parts[lp];
+    const HaloDev h = halo_for(c, P, l, dir);
     switch (which) {
-        case 0: *ptr = P.gflag; *rows = P.M; break;
-        case 1: *ptr = P.fired; *rows = P.B; break;
-        case 2: *ptr = P.active; *rows = P.B; break;
+        case 0: *ptr = h.gflag; *rows = P.M; break;
+        case 1: *ptr = h.fired; *rows = P.B; break;
+        case 2: *ptr = h.active; *rows = P.B; break;
         default: CDF_FAIL(CDFGNN_EUSAGE, "which must be 0..2");
+    }
+    return CDFGNN_OK;
+}
+
+extern "C" int cdfgnn_msg_view(cdfgnn_ctx* c, int32_t lp, int32_t phase, int32_t src, cdfgnn_msg_view_t* out) {
+    if (!c || !out) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
+    if (lp < 0 || lp >= c->k || phase < 0 || phase > 1 || src < 0 || src >= c->p)
+        CDF_FAIL(CDFGNN_EUSAGE, "bad part/phase/source");
+    const LocalPart& P = c->parts[lp];
+    if (src == P.part) CDF_FAIL(CDFGNN_EUSAGE, "a part sends no messages to itself");
+    std::memset(out, 0, sizeof(*out));
+    const int bits = c->cfg.quant_bits;
+    const int64_t ld = c->last_ld[phase] ? c->last_ld[phase] : c->ldmax;
+    out->quant_bits = bits;
+    out->row_bytes = code_row_bytes(bits, ld);
+    // gather messages at the master are indexed by the halo list (src -> me), scatter messages
+    // at the mirror by the mirror slab of master src (the same list seen from the other side)
+    out->capacity = phase == 0 ? P.capB[src] : P.capA[src];
+    if (c->slot) {
+        out->layout = 1;
+        out->base = phase == 0 ? P.gsrc.base[src] : P.ssrc.base[src];
+        out->hdr_bytes = 16;
+        out->slot_bytes = slot_stride(bits, ld);
+        out->stamp = c->last_stamp[phase];
+    } else {
+        const RegionTab& rt = phase == 0 ? P.grecv_h : P.srecv_h;
+        out->layout = 0;
+        out->base = rt.hdr[src];
+        out->pay = rt.pay[src];
+        out->count = rt.cnt[src];
+        out->hdr_bytes = c->hdr_bytes;
     }
     return CDFGNN_OK;
 }

@@ -2,7 +2,9 @@
 //
 //   T  = H W                  (eq. 1; R5 Â(HW))        A = H,  B = Wᵀ (padded copy)
 //   δ̈  = (S Wᵀ) ⊙ 𝟙[H > 0]    (R3, R6)              A = S,  B = W  (padded copy)
-//   ∇W = Hᵀ S                 (eq. 5; R6), split-K  A = Hᵀ, B = Sᵀ (transposed copies)
+//   ∇W = Hᵀ S                 (eq. 5; R6), split-K  A = H, B = S read in place (MN-major);
+//                                                              K-major transposed copies only with
+//                                                              CDFGNN_WGRAD_KMAJOR=1
 // T = HW and δ̈ feed K-major operands; ∇W reads H and S in place as MN-major operands, which
 // for tf32 the UMMA accepts only in the 128-B swizzle with 32-B atoms (layout type 1, 4 k-rows
 // per atom) — with the plain 128-B swizzle the accumulators came back zero.

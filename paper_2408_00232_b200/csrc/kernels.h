@@ -11,6 +11,14 @@ constexpr int kMaxParts = CDFGNN_MAX_PARTS;
 
 inline int64_t ld_of(int64_t F) { return (F + 3) / 4 * 4; }   // reading R24
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+// Bytes of one message row (kernels_halo.cu): B = 0 fp32 payload (4 ld), B = 8 one byte per
+// code (ld), B = 4 two codes per byte (roundup(ld/2, 4)), B = 16 uint16 codes (2 ld).  Always a
+// multiple of 4; columns F..ld-1 carry zero codes.
+inline int64_t code_row_bytes(int bits, int64_t ld) {
+    return bits == 0 ? 4 * ld : (bits == 8 ? ld : (bits == 4 ? align_up(ld / 2, 4) : 2 * ld));
+}
+// Slot-addressed message layout: 16-byte header {u32 stamp, f32 lo, f32 hi, 0} + the row.
+inline int64_t slot_stride(int bits, int64_t ld) { return align_up(16 + code_row_bytes(bits, ld), 16); }
 
 // Message regions of one part, one per peer part.  A region of capacity C holds
 //   hdr: C entries of {u32 pos, f32 lo, f32 hi} (quantised) or {u32 pos} (fp32)
@@ -25,7 +33,7 @@ struct RegionTab {
 struct HaloDev {
     int32_t me, p;
     int64_t n, B, M;
-    int quant;                 // 0 or 8 bits
+    int quant;                 // bits per code: 0 (fp32 payloads), 4, 8 or 16
     int64_t hdr_bytes;         // 12 (quantised) or 4
     const int64_t* moff;       // [p+1] mirror slab offsets (mirror index space)
     const int64_t* hoff;       // [p+1] halo list offsets (master side)
@@ -44,6 +52,15 @@ struct HaloDev {
     float* stage_lohi;         // [B*2]
     float* stage_a;            // [B*ldmax] aggregate for the no-cache fp32 scatter
     int32_t* err;              // protocol error flag (device)
+    const int32_t* hpos;       // [B*p] slot layout: position of master row r in the halo list
+                               // shared with part s (hpos[r*p + s]; -1: no replica on s)
+};
+
+// Slot-addressed message regions (kernels_halo.cu): base[s] = the region of the (this part,
+// peer s) pair in the current phase's direction; slot k at base + k * stride holds the
+// message of the vertex at halo-list position k.  nullptr for s == me.
+struct SlotTab {
+    uint8_t* base[kMaxParts];
 };
 
 // NVLink put: copy each peer's compacted messages (count from device memory) from local
@@ -87,6 +104,10 @@ struct SyncArgs {
     float eps;
     int nocache;          // reading R14
     int no_msgs;          // gather phase elided (§8 f2): masters see no received messages
+    int no_scatter;       // scatter phase elided (§8 f2): masters store no scatter messages
+    int64_t rowb;         // code_row_bytes(quant, ld)
+    int64_t stride;       // slot layout: slot_stride(quant, ld)
+    uint32_t gstamp, sstamp;   // slot layout: stamps of this sync's gather / scatter messages
     CacheDev c;
     unsigned long long* stats;  // [4]: gather_sent, master_fired, active, scatter_msgs
 };
@@ -103,6 +124,13 @@ int launch_map(const HaloDev& h, const RegionTab& rt, int mirror_side, int64_t m
 int launch_master(const HaloDev& h, const SyncArgs& a, const RegionTab& rt, cudaStream_t s);
 int launch_scatter_pack_n(const HaloDev& h, const SyncArgs& a, int ntiles, cudaStream_t s);
 int launch_mirror_apply(const HaloDev& h, const SyncArgs& a, const RegionTab& rt, cudaStream_t s);
+// slot layout: gather stores each sender's message into dst.base[master part] slot pos; the
+// master kernel applies src (gather) slots, its own Δ, and stores the scatter messages into
+// sdst.base[mirror part]; the mirror kernel applies src (scatter) slots
+int launch_gather_slot(const HaloDev& h, const SyncArgs& a, const SlotTab& dst, cudaStream_t s);
+int launch_master_slot(const HaloDev& h, const SyncArgs& a, const SlotTab& src, const SlotTab& sdst,
+                       cudaStream_t s);
+int launch_mirror_slot(const HaloDev& h, const SyncArgs& a, const SlotTab& src, cudaStream_t s);
 
 // ---- SpMM (kernels_spmm.cu): Y[n x ld] = Â T
 // Work items in visiting order: {row, seg} (seg = -1: the whole row; else segment seg of a
@@ -113,14 +141,16 @@ struct SpmmItems {
     const int2* items;          // [n_items]
     const int4* split;          // [n]
     const int32_t* seg_beg;     // [segments + split rows]
-    float* partial;             // [slots x ld] segment partials
+    float* partial;             // [slots x width] segment partials
     int32_t* counter;           // [slots] segments finished per split row (at its first slot; zero at rest)
 };
 int spmm_chunk(bool wide, int64_t nnz);
 int spmm_default_phases();
 int spmm_phase_min_degree();
+// width (<= 1024, % 4 == 0; default ld): the columns computed; ld: row stride of T and Y.  Split-row
+// partials are width floats per slot.
 void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val, int64_t n_items,
-                 const SpmmItems& it, const float* T, float* Y, int64_t ld, cudaStream_t s);
+                 const SpmmItems& it, const float* T, float* Y, int64_t ld, cudaStream_t s, int64_t width = 0);
 
 // ---- dense (kernels_dense.cu)
 // C[M x ldc] = op(A) op(B) (+ mask) ; columns [N, ldc) of C are written as zero.
@@ -158,8 +188,9 @@ void launch_loss(const float* logits, int64_t ld, int C, int64_t n, int64_t B, i
 void launch_reduce_rows(const float* rowloss, int64_t n, double* out, cudaStream_t s);
 void launch_count_train(int64_t n, int64_t B, int64_t M, const uint8_t* train, int* out,
                         cudaStream_t s);
+// err (device, may be NULL): the update is skipped when *err != 0 (protocol / data error)
 void launch_optimizer(int kind, float* W, const float* G, float* m, float* v, int64_t count,
                       float lr, float b1, float b2, float eps, float bc1, float bc2,
-                      cudaStream_t s);
+                      const int32_t* err, cudaStream_t s);
 
 }  // namespace cdfgnn

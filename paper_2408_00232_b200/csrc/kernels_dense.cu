@@ -242,9 +242,11 @@ __global__ void count_train_kernel(int64_t n, int64_t B, int64_t M, const uint8_
 
 __global__ void optimizer_kernel(int kind, float* __restrict__ W, const float* __restrict__ G,
                                  float* __restrict__ m, float* __restrict__ v, int64_t count,
-                                 float lr, float b1, float b2, float eps, float bc1, float bc2) {
+                                 float lr, float b1, float b2, float eps, float bc1, float bc2,
+                                 const int32_t* __restrict__ err) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= count) return;
+    if (err && *err) return;      // a halo / data error this epoch (max over ranks): W stays unchanged
     const float g = G[i];
     if (kind == 0) {
         W[i] = W[i] - lr * g;
@@ -364,10 +366,10 @@ void launch_count_train(int64_t n, int64_t B, int64_t M, const uint8_t* train, i
 
 void launch_optimizer(int kind, float* W, const float* G, float* m, float* v, int64_t count,
                       float lr, float b1, float b2, float eps, float bc1, float bc2,
-                      cudaStream_t s) {
+                      const int32_t* err, cudaStream_t s) {
     if (count <= 0) return;
     optimizer_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(kind, W, G, m, v, count, lr,
-                                                                     b1, b2, eps, bc1, bc2);
+                                                                     b1, b2, eps, bc1, bc2, err);
 }
 
 }  // namespace cdfgnn

@@ -31,74 +31,110 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kScatterTile = 256;
 
-// ---- R15 canonical quantiser (B = 8) ------------------------------------------
-// code = min(floor(RN(RN(RN(RN(d − lo)·256) / rng) + 0.5)), 255), 0 when rng = 0.
-// Fast path: y = RN(t·RN(1/rng)) is within 2^-15 of t/rng (t/rng ∈ [0, 256]), so
-// v = RN(y + 0.5) is within 2^-13 of the canonical RN(RN(t/rng) + 0.5); whenever v's
+// ---- R15 canonical quantiser (B = 4, 8 or 16 bits) ---------------------------
+// code = min(floor(RN(RN(RN(RN(d − lo)·2^B) / rng) + 0.5)), 2^B − 1), 0 when rng = 0.
+// Fast path (B <= 8): y = RN(t·RN(1/rng)) is within a few ulp(2^B) of t/rng (t/rng ∈ [0, 2^B]),
+// so v = RN(y + 0.5) is within 2^-13 of the canonical RN(RN(t/rng) + 0.5); whenever v's
 // fractional part is at least 2^-11 away from an integer both floors agree.  Closer to a
 // boundary the canonical IEEE division decides, so every code is bit-identical to the
-// oracle's fp32 replay (oracle/cache.py) — one reciprocal per row instead of one division
-// per element.
+// oracle's fp32 replay (oracle/quant.py quantize_f32) — one reciprocal per row instead of one
+// division per element.  B = 16: ulp(2^16) = 2^-7 leaves no such margin, every code divides.
 struct QRow {
     float lo, rng, rinv;   // rinv = 0 when rng = 0: the fast path then yields code 0
+    float scale;           // 2^B (exact)
+    float qmax;            // 2^B − 1
+    int bits;
 };
-__device__ __forceinline__ QRow qrow(float lo, float hi) {
+__device__ __forceinline__ QRow qrow(float lo, float hi, int bits) {
     QRow q;
     q.lo = lo;
     q.rng = __fsub_rn(hi, lo);
     q.rinv = q.rng == 0.f ? 0.f : __frcp_rn(q.rng);
+    q.scale = (float)(1u << bits);
+    q.qmax = (float)((1u << bits) - 1u);
+    q.bits = bits;
     return q;
 }
 // fast-path floor of RN(RN(t/rng) + 0.5); *slow is set when the canonical division must decide
-__device__ __forceinline__ float q8_fast(float d, const QRow& q, bool* slow) {
-    const float t = __fmul_rn(__fsub_rn(d, q.lo), 256.f);
+__device__ __forceinline__ float q_fast(float d, const QRow& q, bool* slow) {
+    const float t = __fmul_rn(__fsub_rn(d, q.lo), q.scale);
     const float v = __fadd_rn(__fmul_rn(t, q.rinv), 0.5f);
     const float fl = floorf(v);
     const float fr = __fsub_rn(v, fl);
     *slow = !(fr > 0.00048828125f && fr < 0.99951171875f);      // within 2^-11 of an integer
     return fl;
 }
-__device__ __noinline__ float q8_slow(float d, const QRow& q) {
+__device__ __noinline__ float q_slow(float d, const QRow& q) {
     if (q.rng == 0.f) return 0.f;
-    const float t = __fmul_rn(__fsub_rn(d, q.lo), 256.f);
+    const float t = __fmul_rn(__fsub_rn(d, q.lo), q.scale);
     return floorf(__fadd_rn(__fdiv_rn(t, q.rng), 0.5f));
 }
 // 4 codes of one float4 chunk; the (rare) canonical division runs only for flagged elements
-__device__ __forceinline__ void q8x4(const float (&d)[4], const QRow& q, uint32_t (&c)[4]) {
+__device__ __forceinline__ void qx4(const float (&d)[4], const QRow& q, uint32_t (&c)[4]) {
     float fl[4];
-    bool sl[4], any = false;
+    if (q.bits > 8) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        fl[k] = q8_fast(d[k], q, &sl[k]);
-        any |= sl[k];
+        for (int k = 0; k < 4; ++k) fl[k] = q_slow(d[k], q);
+    } else {
+        bool sl[4], any = false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            fl[k] = q_fast(d[k], q, &sl[k]);
+            any |= sl[k];
+        }
+        if (any) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (sl[k]) fl[k] = q_slow(d[k], q);
+        }
     }
-    if (any) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (sl[k]) fl[k] = q8_slow(d[k], q);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) c[k] = (uint32_t)fminf(fl[k], 255.f);
+    for (int k = 0; k < 4; ++k) c[k] = (uint32_t)fminf(fl[k], q.qmax);
 }
-__device__ __forceinline__ float dq8(uint32_t q, float lo, float step) {
+// dequantisation m̃ = RN(RN(step·q) + lo), step = RN((hi − lo)·2^-B)  (R15)
+__device__ __forceinline__ float dqv(uint32_t q, float lo, float step) {
     return __fadd_rn(__fmul_rn(step, (float)q), lo);
 }
-__device__ __forceinline__ float step8(float lo, float hi) {
-    return __fmul_rn(__fsub_rn(hi, lo), 0.00390625f);   // RN((hi−lo)·2^-8)
+__device__ __forceinline__ float stepq(float lo, float hi, int bits) {
+    return __fmul_rn(__fsub_rn(hi, lo), 1.0f / (float)(1u << bits));   // 2^-B exact
 }
 
-// 4 consecutive uint8 codes at column c0 of a code row.  Code rows are ld = roundup(F, 4)
-// bytes long (padding codes are 0), so every group of 4 is one aligned 32-bit access.
-__device__ __forceinline__ void load_codes4(const uint8_t* row, int c0, uint32_t (&q)[4]) {
-    const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(row + c0));
-    q[0] = w & 0xFFu; q[1] = (w >> 8) & 0xFFu; q[2] = (w >> 16) & 0xFFu; q[3] = w >> 24;
-}
-__device__ __forceinline__ void store_codes4(uint8_t* row, int c0, int F, const uint32_t (&q)[4]) {
-    uint32_t w = 0;
+// Code rows (kernels.h code_row_bytes): B = 8 one byte per code, B = 4 two codes per byte
+// (code k in the low nibble of byte k/2 for even k), B = 16 one little-endian uint16 per code;
+// the F codes are followed by zero padding.  Every group of 4 codes at column c0 (c0 % 4 = 0)
+// is one aligned 16-, 32- or 64-bit access.
+__device__ __forceinline__ void pack_codes4(const uint32_t (&q)[4], int c0, int F, int bits, uint32_t (&w)[2]) {
+    uint32_t m[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-        if (c0 + k < F) w |= q[k] << (8 * k);
-    *reinterpret_cast<uint32_t*>(row + c0) = w;
+    for (int k = 0; k < 4; ++k) m[k] = (c0 + k < F) ? q[k] : 0u;
+    if (bits == 8) { w[0] = m[0] | (m[1] << 8) | (m[2] << 16) | (m[3] << 24); w[1] = 0; }
+    else if (bits == 4) { w[0] = m[0] | (m[1] << 4) | (m[2] << 8) | (m[3] << 12); w[1] = 0; }
+    else { w[0] = m[0] | (m[1] << 16); w[1] = m[2] | (m[3] << 16); }
+}
+__device__ __forceinline__ void put_codes4(uint8_t* row, int c0, int bits, const uint32_t (&w)[2]) {
+    if (bits == 8) *reinterpret_cast<uint32_t*>(row + c0) = w[0];
+    else if (bits == 4) *reinterpret_cast<uint16_t*>(row + c0 / 2) = (uint16_t)w[0];
+    else *reinterpret_cast<uint2*>(row + 2 * c0) = make_uint2(w[0], w[1]);
+}
+__device__ __forceinline__ void store_codes4(uint8_t* row, int c0, int F, const uint32_t (&q)[4], int bits) {
+    uint32_t w[2];
+    pack_codes4(q, c0, F, bits, w);
+    put_codes4(row, c0, bits, w);
+}
+__device__ __forceinline__ void unpack_codes4(const uint32_t (&w)[2], int bits, uint32_t (&q)[4]) {
+    if (bits == 8) { q[0] = w[0] & 0xFFu; q[1] = (w[0] >> 8) & 0xFFu; q[2] = (w[0] >> 16) & 0xFFu; q[3] = w[0] >> 24; }
+    else if (bits == 4) { q[0] = w[0] & 0xFu; q[1] = (w[0] >> 4) & 0xFu; q[2] = (w[0] >> 8) & 0xFu; q[3] = (w[0] >> 12) & 0xFu; }
+    else { q[0] = w[0] & 0xFFFFu; q[1] = w[0] >> 16; q[2] = w[1] & 0xFFFFu; q[3] = w[1] >> 16; }
+}
+__device__ __forceinline__ void fetch_codes4(const uint8_t* row, int c0, int bits, uint32_t (&w)[2]) {
+    if (bits == 8) { w[0] = __ldg(reinterpret_cast<const uint32_t*>(row + c0)); w[1] = 0; }
+    else if (bits == 4) { w[0] = __ldg(reinterpret_cast<const unsigned short*>(row + c0 / 2)); w[1] = 0; }
+    else { const uint2 v = __ldg(reinterpret_cast<const uint2*>(row + 2 * c0)); w[0] = v.x; w[1] = v.y; }
+}
+__device__ __forceinline__ void load_codes4(const uint8_t* row, int c0, int bits, uint32_t (&q)[4]) {
+    uint32_t w[2];
+    fetch_codes4(row, c0, bits, w);
+    unpack_codes4(w, bits, q);
 }
 
 template <int LPR>
@@ -235,15 +271,15 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 2 : 1) gather_pack_kernel
         const int64_t mrow = s_moff[seg] + ridx[r];
         float* sr = a.nocache ? nullptr : a.c.s_mir + mrow * a.ld;
         if (h.quant) {
-            const QRow qr = qrow(lo[r], hi[r]);
-            const float stp = step8(lo[r], hi[r]);
+            const QRow qr = qrow(lo[r], hi[r], h.quant);
+            const float stp = stepq(lo[r], hi[r], h.quant);
             if (gl == 0) {
                 uint32_t* hp = reinterpret_cast<uint32_t*>(hdr + mm * 12);
                 hp[0] = (uint32_t)ridx[r];
                 hp[1] = __float_as_uint(lo[r]);
                 hp[2] = __float_as_uint(hi[r]);
             }
-            uint8_t* codes = pay + mm * a.ld;
+            uint8_t* codes = pay + mm * a.rowb;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
@@ -254,13 +290,13 @@ __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 2 : 1) gather_pack_kernel
                 float dd[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) dd[k] = __fsub_rn(comp(xs[r][v], k), comp(s4, k));
-                q8x4(dd, qr, q);
+                qx4(dd, qr, q);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const float sk = (c0 + k < a.F) ? __fadd_rn(comp(s4, k), dq8(q[k], lo[r], stp)) : 0.f;
+                    const float sk = (c0 + k < a.F) ? __fadd_rn(comp(s4, k), dqv(q[k], lo[r], stp)) : 0.f;
                     setc(snew, k, sk);
                 }
-                store_codes4(codes, c0, a.F, q);
+                store_codes4(codes, c0, a.F, q, h.quant);
                 if (sr) __stcs(reinterpret_cast<float4*>(sr + c0), snew);   // reading R11: s ← s + deq(q(Δ))
             }
         } else {
@@ -350,18 +386,18 @@ __device__ __forceinline__ void master_row(const HaloDev& h, const SyncArgs& a, 
         any_msg = true;
         const uint8_t* pay = rt.pay[s];
         if (h.quant) {
-            const float stp = step8(lo, hi);
-            const uint8_t* codes = pay + (int64_t)m * a.ld;
+            const float stp = stepq(lo, hi, h.quant);
+            const uint8_t* codes = pay + (int64_t)m * a.rowb;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
                 if (c0 >= a.F) continue;
                 uint32_t q[4];
-                load_codes4(codes, c0, q);
+                load_codes4(codes, c0, h.quant, q);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     if (c0 + k < a.F)
-                        setc(acc[v], k, __fadd_rn(comp(acc[v], k), dq8(q[k], lo, stp)));
+                        setc(acc[v], k, __fadd_rn(comp(acc[v], k), dqv(q[k], lo, stp)));
             }
         } else {
             const float* prow = reinterpret_cast<const float*>(pay) + (int64_t)m * a.ld;
@@ -434,9 +470,9 @@ __device__ __forceinline__ void master_row(const HaloDev& h, const SyncArgs& a, 
     }
     if (act) {
         if (h.quant) {
-            const QRow qr = qrow(lo, hi);
-            const float stp = step8(lo, hi);
-            uint8_t* codes = h.stage_codes + r * a.ld;
+            const QRow qr = qrow(lo, hi, h.quant);
+            const float stp = stepq(lo, hi, h.quant);
+            uint8_t* codes = h.stage_codes + r * a.rowb;
             if (gl == 0) { h.stage_lohi[2 * r] = lo; h.stage_lohi[2 * r + 1] = hi; }
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
@@ -444,11 +480,11 @@ __device__ __forceinline__ void master_row(const HaloDev& h, const SyncArgs& a, 
                 if (c0 >= a.F) continue;
                 uint32_t q[4];
                 const float dd[4] = {del[v].x, del[v].y, del[v].z, del[v].w};
-                q8x4(dd, qr, q);
+                qx4(dd, qr, q);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    if (c0 + k < a.F) setc(b[v], k, __fadd_rn(comp(b[v], k), dq8(q[k], lo, stp)));
-                store_codes4(codes, c0, a.F, q);
+                    if (c0 + k < a.F) setc(b[v], k, __fadd_rn(comp(b[v], k), dqv(q[k], lo, stp)));
+                store_codes4(codes, c0, a.F, q, h.quant);
             }
         } else {
 #pragma unroll
@@ -572,8 +608,8 @@ __global__ void __launch_bounds__(kThreads) scatter_pack_kernel(HaloDev h, SyncA
     // (message, word) with coalesced stores
     // (4 independent loads in flight per thread before the stores: the copy is latency-bound)
     if (h.quant) {
-        const int wpr = (int)(a.ld >> 2);        // code rows are ld bytes
-        uint32_t* dst = reinterpret_cast<uint32_t*>(pay + m0 * a.ld);
+        const int wpr = (int)(a.rowb >> 2);      // code rows are rowb bytes (multiple of 4)
+        uint32_t* dst = reinterpret_cast<uint32_t*>(pay + m0 * a.rowb);
         const int nw = total * wpr;
         for (int i0 = threadIdx.x; i0 < nw; i0 += 4 * kThreads) {
             uint32_t w[4];
@@ -581,7 +617,7 @@ __global__ void __launch_bounds__(kThreads) scatter_pack_kernel(HaloDev h, SyncA
             for (int u = 0; u < 4; ++u) {
                 const int i = i0 + u * kThreads;
                 const int k = i / wpr, o = i - k * wpr;
-                w[u] = i < nw ? __ldg(reinterpret_cast<const uint32_t*>(h.stage_codes + (int64_t)s_row[min(k, total - 1)] * a.ld) + o) : 0u;
+                w[u] = i < nw ? __ldg(reinterpret_cast<const uint32_t*>(h.stage_codes + (int64_t)s_row[min(k, total - 1)] * a.rowb) + o) : 0u;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
@@ -638,18 +674,18 @@ __global__ void __launch_bounds__(kThreads) mirror_apply_kernel(HaloDev h, SyncA
         if (h.quant) {
             const uint32_t* hp = reinterpret_cast<const uint32_t*>(hdr + (int64_t)m * 12);
             const float lo = __uint_as_float(__ldg(hp + 1)), hi = __uint_as_float(__ldg(hp + 2));
-            const float stp = step8(lo, hi);
-            const uint8_t* codes = pay + (int64_t)m * a.ld;
+            const float stp = stepq(lo, hi, h.quant);
+            const uint8_t* codes = pay + (int64_t)m * a.rowb;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
                 if (c0 >= a.F) continue;
                 uint32_t q[4];
-                load_codes4(codes, c0, q);
+                load_codes4(codes, c0, h.quant, q);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     if (c0 + k < a.F)
-                        setc(b[v], k, __fadd_rn(comp(b[v], k), dq8(q[k], lo, stp)));
+                        setc(b[v], k, __fadd_rn(comp(b[v], k), dqv(q[k], lo, stp)));
             }
         } else {
             const float* prow = reinterpret_cast<const float*>(pay) + (int64_t)m * a.ld;
@@ -734,6 +770,410 @@ __global__ void nvl_barrier_kernel(const __grid_constant__ BarTab t, uint64_t se
         }
     }
     __threadfence_system();   // acquire: the peer's stores before its release are visible
+}
+
+// ==================================================================================
+// Slot-addressed exchange (co-resident parts and the NVLink push transport; kernels.h
+// SlotTab).  The message of the vertex at halo-list position pos travels in slot pos of
+// the (source -> destination) region: a 16-byte header {u32 stamp, f32 lo, f32 hi, 0}
+// followed by the code row (or the fp32 row).  stamp = the phase's sequence number, so the
+// receiver tells this phase's messages from stale slots without counts, prefix sums, range
+// reservations or index maps, and the sender stores straight into the receiver's region
+// (through the CUDA-IPC mapping when it lives on a peer GPU: no local staging, no copy pass).
+// ==================================================================================
+__device__ __forceinline__ uint4 ld_hdr(const uint8_t* slot) {
+    return __ldg(reinterpret_cast<const uint4*>(slot));
+}
+__device__ __forceinline__ void st_hdr(uint8_t* slot, uint32_t stamp, float lo, float hi) {
+    *reinterpret_cast<uint4*>(slot) = make_uint4(stamp, __float_as_uint(lo), __float_as_uint(hi), 0u);
+}
+
+// gather (Alg. 2 L3-L9): RPW row groups per warp pass, one mirror row per group
+template <int LPR, int VPL, int RPW>
+__global__ void __launch_bounds__(kThreads, VPL <= 2 ? 2 : 1)
+gather_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab dst) {
+    constexpr int GPW = 32 / LPR;
+    __shared__ int64_t s_moff[kMaxParts + 1];
+    __shared__ unsigned s_cnt;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x <= h.p) s_moff[threadIdx.x] = h.moff[threadIdx.x];
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const int g = lane / LPR, gl = lane % LPR;
+    const int64_t row0 = ((int64_t)blockIdx.x * kWarps + warp) * RPW * GPW;
+    float4 xs[RPW][VPL], ss[RPW][VPL];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+        const int64_t row = row0 + r * GPW + g;
+        const bool valid = row < h.M;
+        const float* xr = a.X + (h.B + (valid ? row : 0)) * a.ld;
+        const float* sr = a.nocache ? nullptr : a.c.s_mir + (valid ? row : 0) * a.ld;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+            const int c0 = (gl + v * LPR) * 4;
+            xs[r][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            ss[r][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (valid && c0 < a.ld) {
+                xs[r][v] = __ldcs(reinterpret_cast<const float4*>(xr + c0));   // read once
+                if (sr) ss[r][v] = __ldcs(reinterpret_cast<const float4*>(sr + c0));
+            }
+        }
+    }
+    unsigned sent = 0;
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+        const int64_t row = row0 + r * GPW + g;
+        const bool valid = row < h.M;
+        float maxs = 0.f, lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+            const int c0 = (gl + v * LPR) * 4;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float dk = __fsub_rn(comp(xs[r][v], k), comp(ss[r][v], k));
+                if (c0 + k < a.F) {
+                    maxs = fmaxf(maxs, fabsf(comp(ss[r][v], k)));
+                    lo = fminf(lo, dk);
+                    hi = fmaxf(hi, dk);
+                }
+            }
+        }
+        maxs = gmax<LPR>(maxs);
+        lo = gmin<LPR>(lo);
+        hi = gmax<LPR>(hi);
+        // ‖d‖∞ = max(|min d|, |max d|): exact; the test of Alg. 2 L4 (reading R15)
+        const float maxd = valid ? fmaxf(fabsf(lo), fabsf(hi)) : 0.f;
+        const bool flag = valid && (a.nocache || maxd > __fmul_rn(a.eps, maxs));
+        sent += __popc(__ballot_sync(0xffffffffu, flag && gl == 0));
+        if (valid && gl == 0) h.gflag[row] = flag ? 1 : 0;
+        if (!flag) continue;
+        const int q = find_seg(s_moff, h.p, row);
+        uint8_t* slot = dst.base[q] + (row - s_moff[q]) * a.stride;
+        float* sr = a.nocache ? nullptr : a.c.s_mir + row * a.ld;
+        if (h.quant) {
+            const QRow qr = qrow(lo, hi, h.quant);
+            const float stp = stepq(lo, hi, h.quant);
+            if (gl == 0) st_hdr(slot, a.gstamp, lo, hi);
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 >= a.F) continue;
+                uint32_t qc[4];
+                float dd[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) dd[k] = __fsub_rn(comp(xs[r][v], k), comp(ss[r][v], k));
+                qx4(dd, qr, qc);
+                store_codes4(slot + 16, c0, a.F, qc, h.quant);
+                if (sr) {
+                    float4 snew;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        setc(snew, k, (c0 + k < a.F) ? __fadd_rn(comp(ss[r][v], k), dqv(qc[k], lo, stp)) : 0.f);
+                    __stcs(reinterpret_cast<float4*>(sr + c0), snew);   // reading R11: s ← s + deq(q(Δ))
+                }
+            }
+        } else {
+            if (gl == 0) st_hdr(slot, a.gstamp, 0.f, 0.f);
+            float* prow = reinterpret_cast<float*>(slot + 16);
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 >= a.ld) continue;
+                float4 dv;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) setc(dv, k, __fsub_rn(comp(xs[r][v], k), comp(ss[r][v], k)));
+                st4(prow + c0, dv);
+                if (sr) st4(sr + c0, xs[r][v]);   // Alg. 2 L6: s ← z
+            }
+        }
+    }
+    if (lane == 0 && sent) atomicAdd(&s_cnt, sent);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_cnt) atomicAdd(&a.stats[0], (unsigned long long)s_cnt);
+    if (h.remote) __threadfence_system();   // stored into peer GPUs: visible before the barrier
+}
+
+// master apply + scatter (Alg. 2 L10-L22): one row group per boundary master row.  Lane s of
+// the group holds the row's slot in the halo list shared with part s (static, -1: no replica
+// on s) — the slot its gather message arrives in and the slot its scatter message goes to.
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(kThreads, VPL <= 2 ? 4 : 1)
+master_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab src, const __grid_constant__ SlotTab sdst) {
+    constexpr int GPW = 32 / LPR;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / LPR, gl = lane % LPR;
+    const int64_t row = ((int64_t)blockIdx.x * kWarps + warp) * GPW + g;
+    const bool valid = row < h.B;
+    const int64_t r = valid ? row : 0;
+    const int p = h.p;
+    const bool lanes_hold = p <= LPR;
+    // independent loads first: the row's slots, aggregate, own value, snapshot, scatter base
+    int32_t hp = -1;
+    if (lanes_hold && valid && gl < p && gl != h.me) hp = __ldg(h.hpos + r * p + gl);
+    float* xr = a.X + r * a.ld;
+    float* smr = a.nocache ? nullptr : a.c.s_mas + r * a.ld;
+    float* bmr = a.nocache ? nullptr : a.c.b_mas + r * a.ld;
+    float* ar = a.nocache ? nullptr : a.c.a + r * a.ld;
+    float4 acc[VPL], x[VPL], s4v[VPL], b[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+        const int c0 = (gl + v * LPR) * 4;
+        const bool in = valid && c0 < a.ld;
+        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        acc[v] = (ar && in) ? ld4(ar + c0) : z4;
+        x[v] = in ? ld4(xr + c0) : z4;
+        s4v[v] = (smr && in) ? ld4(smr + c0) : z4;
+        b[v] = (bmr && in) ? ld4(bmr + c0) : z4;
+    }
+    uint4 hd = make_uint4(0u, 0u, 0u, 0u);
+    if (hp >= 0 && !a.no_msgs) hd = ld_hdr(src.base[gl] + (int64_t)hp * a.stride);
+    const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (g * LPR));
+    const unsigned have = (__ballot_sync(0xffffffffu, hp >= 0 && !a.no_msgs && hd.x == a.gstamp) & gmask) >> (g * LPR);
+    const unsigned peers = (__ballot_sync(0xffffffffu, hp >= 0) & gmask) >> (g * LPR);
+    bool any_msg = false;
+    // Alg. 2 L11-L13: received Δ in ascending source part (R13)
+    for (int s = 0; s < p; ++s) {
+        if (s == h.me) continue;
+        int32_t hps;
+        float lo = 0.f, hi = 0.f;
+        if (lanes_hold) {
+            if (!((have >> s) & 1u)) continue;
+            hps = __shfl_sync(gmask, hp, g * LPR + s);
+            lo = __uint_as_float(__shfl_sync(gmask, hd.y, g * LPR + s));
+            hi = __uint_as_float(__shfl_sync(gmask, hd.z, g * LPR + s));
+        } else {
+            hps = (valid && !a.no_msgs) ? __ldg(h.hpos + r * p + s) : -1;
+            if (hps < 0) continue;
+            const uint4 hs = ld_hdr(src.base[s] + (int64_t)hps * a.stride);
+            if (hs.x != a.gstamp) continue;
+            lo = __uint_as_float(hs.y);
+            hi = __uint_as_float(hs.z);
+        }
+        any_msg = true;
+        const uint8_t* pay = src.base[s] + (int64_t)hps * a.stride + 16;
+        if (h.quant) {
+            const float stp = stepq(lo, hi, h.quant);
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 >= a.F) continue;
+                uint32_t qc[4];
+                load_codes4(pay, c0, h.quant, qc);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (c0 + k < a.F) setc(acc[v], k, __fadd_rn(comp(acc[v], k), dqv(qc[k], lo, stp)));
+            }
+        } else {
+            const float* prow = reinterpret_cast<const float*>(pay);
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 >= a.ld) continue;
+                const float4 pv = ld4(prow + c0);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) setc(acc[v], k, __fadd_rn(comp(acc[v], k), comp(pv, k)));
+            }
+        }
+    }
+    // Alg. 2 L14-L19: the master's own replica, unquantised
+    float4 dd[VPL];
+    float maxd = 0.f, maxs = 0.f;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+        const int c0 = (gl + v * LPR) * 4;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float dk = __fsub_rn(comp(x[v], k), comp(s4v[v], k));
+            setc(dd[v], k, dk);
+            if (c0 + k < a.F) {
+                maxd = fmaxf(maxd, fabsf(dk));
+                maxs = fmaxf(maxs, fabsf(comp(s4v[v], k)));
+            }
+        }
+    }
+    maxd = gmax<LPR>(maxd);
+    maxs = gmax<LPR>(maxs);
+    const bool fired = valid && (a.nocache || maxd > __fmul_rn(a.eps, maxs));
+    if (fired) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+            const int c0 = (gl + v * LPR) * 4;
+            if (c0 >= a.ld) continue;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) setc(acc[v], k, __fadd_rn(comp(acc[v], k), comp(dd[v], k)));
+            if (smr) st4(smr + c0, x[v]);
+        }
+    }
+    const bool act = valid && (fired || any_msg);
+    if (act && ar) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+            const int c0 = (gl + v * LPR) * 4;
+            if (c0 < a.ld) st4(ar + c0, acc[v]);
+        }
+    }
+    // Alg. 2 L20-L22 / R12: the scatter delta a − b quantised once; every replica applies the
+    // same codes (range reduced by every lane of the warp: shuffles stay converged)
+    float lo = INFINITY, hi = -INFINITY;
+    float4 del[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+        const int c0 = (gl + v * LPR) * 4;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float dk = __fsub_rn(comp(acc[v], k), comp(b[v], k));
+            setc(del[v], k, dk);
+            if (c0 + k < a.F) { lo = fminf(lo, dk); hi = fmaxf(hi, dk); }
+        }
+    }
+    if (h.quant) {
+        lo = gmin<LPR>(lo);
+        hi = gmax<LPR>(hi);
+    }
+    int nmsg = 0;
+    if (act) {
+        uint32_t pk[VPL][2];
+        if (h.quant) {
+            const QRow qr = qrow(lo, hi, h.quant);
+            const float stp = stepq(lo, hi, h.quant);
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                pk[v][0] = pk[v][1] = 0u;
+                if (c0 >= a.F) continue;
+                uint32_t qc[4];
+                const float d4[4] = {del[v].x, del[v].y, del[v].z, del[v].w};
+                qx4(d4, qr, qc);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (c0 + k < a.F) setc(b[v], k, __fadd_rn(comp(b[v], k), dqv(qc[k], lo, stp)));
+                pack_codes4(qc, c0, a.F, h.quant, pk[v]);
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) b[v] = acc[v];
+        }
+        if (bmr) {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 < a.ld) st4(bmr + c0, b[v]);
+            }
+        }
+        // one message per mirror peer, stored straight into its slot
+        if (!a.no_scatter) {
+            for (int s = 0; s < p; ++s) {
+                if (s == h.me) continue;
+                int32_t hps;
+                if (lanes_hold) {
+                    if (!((peers >> s) & 1u)) continue;
+                    hps = __shfl_sync(gmask, hp, g * LPR + s);
+                } else {
+                    hps = __ldg(h.hpos + r * p + s);
+                    if (hps < 0) continue;
+                }
+                uint8_t* slot = sdst.base[s] + (int64_t)hps * a.stride;
+                ++nmsg;
+                if (gl == 0) st_hdr(slot, a.sstamp, lo, hi);
+                if (h.quant) {
+#pragma unroll
+                    for (int v = 0; v < VPL; ++v) {
+                        const int c0 = (gl + v * LPR) * 4;
+                        if (c0 < a.F) put_codes4(slot + 16, c0, h.quant, pk[v]);
+                    }
+                } else {
+                    float* prow = reinterpret_cast<float*>(slot + 16);
+#pragma unroll
+                    for (int v = 0; v < VPL; ++v) {
+                        const int c0 = (gl + v * LPR) * 4;
+                        if (c0 < a.ld) st4(prow + c0, b[v]);
+                    }
+                }
+            }
+        }
+    }
+    if (valid) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+            const int c0 = (gl + v * LPR) * 4;
+            if (c0 < a.ld) st4(xr + c0, b[v]);      // Z row from the cached value
+        }
+        if (gl == 0) {
+            h.fired[r] = fired ? 1 : 0;
+            h.active[r] = act ? 1 : 0;
+        }
+    }
+    const unsigned bf = __ballot_sync(0xffffffffu, fired && gl == 0);
+    const unsigned ba = __ballot_sync(0xffffffffu, act && gl == 0);
+    int ns = (gl == 0) ? nmsg : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
+    if (lane == 0) {
+        if (bf) atomicAdd(&a.stats[1], (unsigned long long)__popc(bf));
+        if (ba) atomicAdd(&a.stats[2], (unsigned long long)__popc(ba));
+        if (ns) atomicAdd(&a.stats[3], (unsigned long long)ns);
+    }
+    if (h.remote) __threadfence_system();
+}
+
+// mirrors receive the scatter: b += deq(q) (or b ← a), Z row ← b
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(kThreads) mirror_slot_kernel(HaloDev h, SyncArgs a,
+                                                               const __grid_constant__ SlotTab src) {
+    constexpr int GPW = 32 / LPR;
+    __shared__ int64_t s_moff[kMaxParts + 1];
+    if (threadIdx.x <= h.p) s_moff[threadIdx.x] = h.moff[threadIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / LPR, gl = lane % LPR;
+    const int64_t row = ((int64_t)blockIdx.x * kWarps + warp) * GPW + g;
+    if (row >= h.M) return;
+    const int q = find_seg(s_moff, h.p, row);
+    const uint8_t* slot = src.base[q] + (row - s_moff[q]) * a.stride;
+    const uint4 hd = ld_hdr(slot);
+    float* bmr = a.nocache ? nullptr : a.c.b_mir + row * a.ld;
+    float4 b[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+        const int c0 = (gl + v * LPR) * 4;
+        b[v] = (bmr && c0 < a.ld) ? ld4(bmr + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (hd.x == a.sstamp) {
+        if (h.quant) {
+            const float lo = __uint_as_float(hd.y), hi = __uint_as_float(hd.z);
+            const float stp = stepq(lo, hi, h.quant);
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 >= a.F) continue;
+                uint32_t qc[4];
+                load_codes4(slot + 16, c0, h.quant, qc);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (c0 + k < a.F) setc(b[v], k, __fadd_rn(comp(b[v], k), dqv(qc[k], lo, stp)));
+            }
+        } else {
+            const float* prow = reinterpret_cast<const float*>(slot + 16);
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 < a.ld) b[v] = ld4(prow + c0);
+            }
+        }
+        if (bmr) {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 < a.ld) st4(bmr + c0, b[v]);
+            }
+        }
+    }
+    float* xr = a.X + (h.B + row) * a.ld;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+        const int c0 = (gl + v * LPR) * 4;
+        if (c0 < a.ld) st4(xr + c0, b[v]);
+    }
 }
 
 // ---- dispatch by row width: LPR lanes x VPL float4 per lane cover ld columns ------
@@ -846,6 +1286,44 @@ int launch_mirror_apply(const HaloDev& h, const SyncArgs& a, const RegionTab& rt
         return (unsigned)((h.M + rows_per_block - 1) / rows_per_block);
     };
     CDF_DISPATCH(a.ld, mirror_apply_kernel, grid, s, h, a, rt);
+    return 1;
+}
+
+int launch_gather_slot(const HaloDev& h, const SyncArgs& a, const SlotTab& dst, cudaStream_t s) {
+    if (h.M <= 0) return 0;
+    const Shape sh = shape_of(a.ld);
+    const int rpw = gather_rpw(sh.lpr, sh.vpl);
+    const int64_t rpb = (int64_t)kWarps * (32 / sh.lpr) * rpw;
+    const unsigned grid = (unsigned)((h.M + rpb - 1) / rpb);
+    if (sh.lpr == 2) gather_slot_kernel<2, 1, 1><<<grid, kThreads, 0, s>>>(h, a, dst);
+    else if (sh.lpr == 4) gather_slot_kernel<4, 1, 1><<<grid, kThreads, 0, s>>>(h, a, dst);
+    else if (sh.lpr == 8 && sh.vpl == 1) gather_slot_kernel<8, 1, 1><<<grid, kThreads, 0, s>>>(h, a, dst);
+    else if (sh.lpr == 8) gather_slot_kernel<8, 2, 2><<<grid, kThreads, 0, s>>>(h, a, dst);
+    else if (sh.vpl == 1) gather_slot_kernel<32, 1, 4><<<grid, kThreads, 0, s>>>(h, a, dst);
+    else if (sh.vpl == 2) gather_slot_kernel<32, 2, 4><<<grid, kThreads, 0, s>>>(h, a, dst);
+    else if (sh.vpl == 4) gather_slot_kernel<32, 4, 2><<<grid, kThreads, 0, s>>>(h, a, dst);
+    else gather_slot_kernel<32, 8, 1><<<grid, kThreads, 0, s>>>(h, a, dst);
+    return 1;
+}
+
+int launch_master_slot(const HaloDev& h, const SyncArgs& a, const SlotTab& src, const SlotTab& sdst,
+                       cudaStream_t s) {
+    if (h.B <= 0) return 0;
+    auto grid = [&](int lpr) {
+        const int64_t rows_per_block = kWarps * (32 / lpr);
+        return (unsigned)((h.B + rows_per_block - 1) / rows_per_block);
+    };
+    CDF_DISPATCH(a.ld, master_slot_kernel, grid, s, h, a, src, sdst);
+    return 1;
+}
+
+int launch_mirror_slot(const HaloDev& h, const SyncArgs& a, const SlotTab& src, cudaStream_t s) {
+    if (h.M <= 0) return 0;
+    auto grid = [&](int lpr) {
+        const int64_t rows_per_block = kWarps * (32 / lpr);
+        return (unsigned)((h.M + rows_per_block - 1) / rows_per_block);
+    };
+    CDF_DISPATCH(a.ld, mirror_slot_kernel, grid, s, h, a, src);
     return 1;
 }
 

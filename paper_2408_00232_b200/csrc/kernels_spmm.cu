@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n_items, const i
                                                         const int32_t* __restrict__ colidx,
                                                         const float* __restrict__ val,
                                                         const float* __restrict__ T,
-                                                        float* __restrict__ Y, int64_t ld,
+                                                        float* __restrict__ Y, int64_t ld, int64_t width,
                                                         SpmmItems it, int stream) {
     constexpr int GPW = 32 / LPR;
     const int lane = threadIdx.x & 31;
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n_items, const i
     for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     bool colok[VPL];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) colok[v] = (gl + v * LPR) * 4 < ld;
+    for (int v = 0; v < VPL; ++v) colok[v] = (gl + v * LPR) * 4 < width;
     for (int base = beg; base < end; base += LPR) {
         const int e = base + gl;
         const int c = e < end ? (stream ? __ldcs(colidx + e) : __ldg(colidx + e)) : 0;
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n_items, const i
         // split row: publish this chunk's partial; the last of the row's chunks to finish
         // sums all partials in chunk order (fixed order => deterministic bits)
         const int pbase = sp.x, nch = sp.y;
-        float* pr = it.partial + (int64_t)(pbase + chunk) * ld;
+        float* pr = it.partial + (int64_t)(pbase + chunk) * width;
 #pragma unroll
         for (int v = 0; v < VPL; ++v)
             if (colok[v]) __stcg(reinterpret_cast<float4*>(pr + (gl + v * LPR) * 4), acc[v]);
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n_items, const i
 #pragma unroll
         for (int v = 0; v < VPL; ++v) sum[v] = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int cc = 0; cc < nch; ++cc) {
-            const float* qr = it.partial + (int64_t)(pbase + cc) * ld;
+            const float* qr = it.partial + (int64_t)(pbase + cc) * width;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 if (!colok[v]) continue;
@@ -191,13 +191,13 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n_items, const i
 
 template <int LPR, int VPL, int UNR>
 void launch(int64_t n, const int32_t* rowptr, const int32_t* colidx, const float* val, const float* T, float* Y,
-            int64_t ld, const SpmmItems& it, cudaStream_t s, int tail, int stream) {
+            int64_t ld, int64_t width, const SpmmItems& it, cudaStream_t s, int tail, int stream) {
     const int64_t rows_per_block = (kThreads / 32) * (32 / LPR);
     const unsigned grid = (unsigned)((n + rows_per_block - 1) / rows_per_block);
     if (tail)
-        spmm_kernel<LPR, VPL, UNR, 1><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, it, stream);
+        spmm_kernel<LPR, VPL, UNR, 1><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream);
     else
-        spmm_kernel<LPR, VPL, UNR, 0><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, it, stream);
+        spmm_kernel<LPR, VPL, UNR, 0><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream);
 }
 
 int env_int(const char* name, int dflt) {
@@ -222,42 +222,43 @@ int spmm_default_phases() { return env_int("CDFGNN_SPMM_PHASES", 1); }
 int spmm_phase_min_degree() { return env_int("CDFGNN_SPMM_PHASE_MIN", 64); }
 
 void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val, int64_t n_items,
-                 const SpmmItems& it, const float* T, float* Y, int64_t ld, cudaStream_t s) {
+                 const SpmmItems& it, const float* T, float* Y, int64_t ld, cudaStream_t s, int64_t width) {
     if (n_items <= 0) return;
-    const int nv = (int)(ld / 4);      // float4 per row
+    if (width <= 0) width = ld;
+    const int nv = (int)(width / 4);   // float4 per row (width % 4 == 0, width <= 1024)
     const int unr = env_int("CDFGNN_SPMM_UNR", 0);
     const int tail = env_int("CDFGNN_SPMM_TAIL", ld > 64 ? 1 : 0);   // predicated tail for wide rows
     // narrow rows: stream the CSR arrays and the output past L2 (evict-first), keeping T's lines
     const int stream = env_int("CDFGNN_SPMM_STREAM", ld <= 64 ? 1 : 0);
-    if (nv <= 2) launch<2, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
-    else if (nv <= 4) launch<4, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
-    else if (nv <= 8) launch<8, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+    if (nv <= 2) launch<2, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+    else if (nv <= 4) launch<4, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+    else if (nv <= 8) launch<8, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
     else if (nv <= 16) {
         // 8 lanes x 2 float4 per row, 8 neighbours in flight, predicated tail batch: at ld = 44
         // (C3's 41 classes) 1.75 -> 1.48 ms per launch vs 16 lanes x 1 (p = 1, tools/spmm_bench.py,
         // profiles/r1); 4x3 and 2x6 were slower (fewer neighbours in flight per lane)
         const int shape = env_int("CDFGNN_SPMM_SHAPE", 3);
-        if (shape == 1 && nv <= 12) launch<4, 3, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
-        else if (shape == 2 && nv <= 12) launch<2, 6, 2>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
-        else if (shape == 3) launch<8, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
-        else if (shape == 4) launch<16, 1, 16>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
-        else if (shape == 5) launch<4, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
-        else if (shape == 6) launch<8, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, 1, stream);
-        else if (unr == 4) launch<16, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
-        else launch<16, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+        if (shape == 1 && nv <= 12) launch<4, 3, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream);
+        else if (shape == 2 && nv <= 12) launch<2, 6, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream);
+        else if (shape == 3) launch<8, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream);
+        else if (shape == 4) launch<16, 1, 16>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream);
+        else if (shape == 5) launch<4, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream);
+        else if (shape == 6) launch<8, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream);
+        else if (unr == 4) launch<16, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+        else launch<16, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
     } else if (nv <= 32) {
-        if (unr == 4) launch<32, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
-        else launch<32, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+        if (unr == 4) launch<32, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+        else launch<32, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
     } else if (nv <= 64) {
         const int wshape = env_int("CDFGNN_SPMM_WSHAPE", 0);
-        if (wshape == 1) launch<16, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
-        else if (wshape == 2) launch<16, 4, 2>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
-        else if (wshape == 3) launch<32, 2, 6>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
-        else if (unr == 2) launch<32, 2, 2>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
-        else if (unr == 8) launch<32, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
-        else launch<32, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
-    } else if (nv <= 128) launch<32, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
-    else launch<32, 8, 2>(n_items, rowptr, colidx, val, T, Y, ld, it, s, tail, stream);
+        if (wshape == 1) launch<16, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+        else if (wshape == 2) launch<16, 4, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+        else if (wshape == 3) launch<32, 2, 6>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+        else if (unr == 2) launch<32, 2, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+        else if (unr == 8) launch<32, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+        else launch<32, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+    } else if (nv <= 128) launch<32, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+    else launch<32, 8, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
 }
 
 }  // namespace cdfgnn

@@ -10,7 +10,11 @@ Recipe:
     Vertex ids are randomly permuted.  Edges are returned once, as (min, max),
     sorted lexicographically.
   * labels: the planted class, uniform over C classes.
-  * features: x_v = mu_{y_v} + N(0, I), mu_c ~ N(0, I), fp32.
+  * features: x_v = snr * mu_{y_v} + N(0, I), mu_c ~ N(0, I), fp32.  ``snr`` (feature
+    signal-to-noise knob, default 1 = the SURVEY §8(d2) recipe) scales the class means:
+    small values (e.g. 0.05 at F_0 = 128) make the classes overlap so train accuracy
+    climbs over tens of epochs instead of saturating at once (used by the adaptive-ε
+    study and the follow-mode trajectory tests; inputs only).
   * masks: train / val / test = 60 / 20 / 20 by a seeded shuffle.
   * weights: Glorot-uniform U(+-sqrt(6/(F_in+F_out))), fp32, [F_in x F_out].
 """
@@ -190,9 +194,11 @@ def glorot_weights(dims, rng: np.random.Generator) -> List[np.ndarray]:
     return out
 
 
-def _features_masks(n, y, f0, classes, rng_f, rng_m):
+def _features_masks(n, y, f0, classes, rng_f, rng_m, snr: float = 1.0):
     mu = rng_f.standard_normal((classes, f0), dtype=np.float32)
     X = rng_f.standard_normal((n, f0), dtype=np.float32)
+    if snr != 1.0:
+        mu *= np.float32(snr)
     X += mu[y]
     perm = rng_m.permutation(n)
     ntr = int(round(0.6 * n))
@@ -203,8 +209,9 @@ def _features_masks(n, y, f0, classes, rng_f, rng_m):
     return X, train, val, test
 
 
-def make_dataset(cfg: GraphConfig, scale: Optional[float] = None) -> Dataset:
-    """Generate a config's dataset.  ``scale`` < 1 shrinks n and nnz (same mean degree)."""
+def make_dataset(cfg: GraphConfig, scale: Optional[float] = None, snr: float = 1.0) -> Dataset:
+    """Generate a config's dataset.  ``scale`` < 1 shrinks n and nnz (same mean degree);
+    ``snr`` scales the feature class means (see the module docstring)."""
     n, m = cfg.n, cfg.m
     v0 = cfg.v0
     if scale is not None and scale != 1.0:
@@ -214,20 +221,23 @@ def make_dataset(cfg: GraphConfig, scale: Optional[float] = None) -> Dataset:
         m = min(m, n * (n - 1) // 4)
     rg, rf, rm, rw = _rngs(cfg.seed)
     eu, ev, y = chung_lu_planted(n, m, cfg.tau, v0, cfg.classes, cfg.homophily, rg)
-    X, train, val, test = _features_masks(n, y, cfg.dims[0], cfg.classes, rf, rm)
+    X, train, val, test = _features_masks(n, y, cfg.dims[0], cfg.classes, rf, rm, snr)
     W = glorot_weights(cfg.dims, rw)
+    name = cfg.key if scale in (None, 1.0) else f"{cfg.key}@{scale}"
+    if snr != 1.0:
+        name += f"/snr{snr}"
     return Dataset(n=n, eu=eu, ev=ev, X=X, y=y, train=train, val=val, test=test,
-                   W=W, dims=tuple(cfg.dims), name=cfg.key if scale in (None, 1.0)
-                   else f"{cfg.key}@{scale}")
+                   W=W, dims=tuple(cfg.dims), name=name)
 
 
 def small_random_graph(n: int, m: int, dims, seed: int, classes: Optional[int] = None,
-                       tau: float = 2.5, v0: float = 1.0, homophily: float = 0.7) -> Dataset:
+                       tau: float = 2.5, v0: float = 1.0, homophily: float = 0.7,
+                       snr: float = 1.0) -> Dataset:
     """A small heavy-tailed dataset for unit tests."""
     classes = classes or dims[-1]
     rg, rf, rm, rw = _rngs(seed)
     eu, ev, y = chung_lu_planted(n, m, tau, v0, classes, homophily, rg)
-    X, train, val, test = _features_masks(n, y, dims[0], classes, rf, rm)
+    X, train, val, test = _features_masks(n, y, dims[0], classes, rf, rm, snr)
     W = glorot_weights(dims, rw)
     return Dataset(n=n, eu=eu, ev=ev, X=X, y=y, train=train, val=val, test=test,
                    W=W, dims=tuple(dims), name=f"rand{n}x{m}")

@@ -62,3 +62,21 @@ def test_two_gpus_full_size_C3_match_unpartitioned():
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert json.loads(lines[-1])["mgpu_check"] == "PASS"
+
+
+@pytest.mark.parametrize("transport", ["push", "nccl"])
+def test_multi_gpu_halo_replay_bitwise_vs_oracle(transport):
+    """One part per GPU (2..4 GPUs): synced rows, cache tables, flags, counters and — NVLink
+    push, slot-addressed — every received message byte equal oracle.cache.sync's fp32 replay
+    (tools/halo_replay_mgpu.py; B ∈ {0, 4, 8, 16}, cache on/off, ε ∈ {0, 0.02, 0.05})."""
+    torch = require_gpu()
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
+           "--master-addr", "127.0.0.1", "--master-port", "29521",
+           os.path.join(ROOT, "tools", "halo_replay_mgpu.py"), "--transport", transport]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert json.loads(lines[-1])["halo_replay"] == "PASS"
