@@ -16,6 +16,6 @@ for l in open(sys.argv[1]):
     if l.startswith("{"):
         d = json.loads(l)
         print(json.dumps({k: d.get(k) for k in ["n_gpus", "value", "phase_ms", "comm_bytes_per_epoch",
-                                                 "remote_accesses_avoided_frac", "loss", "eps", "prep_s"]}))
+                                                 "remote_accesses", "loss", "eps", "prep_s"]}))
 PY
 done

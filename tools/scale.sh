@@ -13,5 +13,5 @@ for N in 1 2 4 8; do
   echo "N=$N rc=$?"; cat gpurun_out/scale_${MODE}_n$N.json | python -c "import json,sys
 for l in sys.stdin:
     if l.startswith('{'):
-        d=json.loads(l); print(json.dumps({k:d.get(k) for k in ['n_gpus','value','phase_ms','comm_bytes_per_epoch','remote_accesses_avoided_frac','nvlink','e2e']}))"
+        d=json.loads(l); print(json.dumps({k:d.get(k) for k in ['n_gpus','value','phase_ms','comm_bytes_per_epoch','remote_accesses','nvlink','e2e']}))"
 done
