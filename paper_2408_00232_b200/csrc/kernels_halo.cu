@@ -40,7 +40,8 @@ constexpr int kScatterTile = 256;
 // oracle's fp32 replay (oracle/quant.py quantize_f32) — one reciprocal per row instead of one
 // division per element.  B = 16: ulp(2^16) = 2^-7 leaves no such margin, every code divides.
 struct QRow {
-    float lo, rng, rinv;   // rinv = 0 when rng = 0: the fast path then yields code 0
+    float lo, rng;
+    float rinv_s;          // RN(1/rng)·2^B (exact scaling); 0 when rng = 0: the fast path yields code 0
     float scale;           // 2^B (exact)
     float qmax;            // 2^B − 1
     int bits;
@@ -49,19 +50,19 @@ __device__ __forceinline__ QRow qrow(float lo, float hi, int bits) {
     QRow q;
     q.lo = lo;
     q.rng = __fsub_rn(hi, lo);
-    q.rinv = q.rng == 0.f ? 0.f : __frcp_rn(q.rng);
     q.scale = (float)(1u << bits);
+    q.rinv_s = q.rng == 0.f ? 0.f : __fmul_rn(__frcp_rn(q.rng), q.scale);
     q.qmax = (float)((1u << bits) - 1u);
     q.bits = bits;
     return q;
 }
-// fast-path floor of RN(RN(t/rng) + 0.5); *slow is set when the canonical division must decide
+// fast-path floor of RN(RN(t/rng) + 0.5); *slow is set when the canonical division must decide.
+// t·RN(1/rng) = RN(d − lo)·2^B·RN(1/rng): the power-of-two factor is exact, so it is applied to
+// the reciprocal once per row (one multiplication per element fewer, same bits).
 __device__ __forceinline__ float q_fast(float d, const QRow& q, bool* slow) {
-    const float t = __fmul_rn(__fsub_rn(d, q.lo), q.scale);
-    const float v = __fadd_rn(__fmul_rn(t, q.rinv), 0.5f);
+    const float v = __fadd_rn(__fmul_rn(__fsub_rn(d, q.lo), q.rinv_s), 0.5f);
     const float fl = floorf(v);
-    const float fr = __fsub_rn(v, fl);
-    *slow = !(fr > 0.00048828125f && fr < 0.99951171875f);      // within 2^-11 of an integer
+    *slow = fabsf(__fsub_rn(__fsub_rn(v, fl), 0.5f)) >= 0.49951171875f;   // within 2^-11 of an integer
     return fl;
 }
 __device__ __noinline__ float q_slow(float d, const QRow& q) {
@@ -789,7 +790,7 @@ __device__ __forceinline__ void st_hdr(uint8_t* slot, uint32_t stamp, float lo, 
 }
 
 // gather (Alg. 2 L3-L9): RPW row groups per warp pass, one mirror row per group
-template <int LPR, int VPL, int RPW>
+template <int LPR, int VPL, int RPW, int QB>
 __global__ void __launch_bounds__(kThreads, VPL <= 2 ? 2 : 1)
 gather_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab dst) {
     constexpr int GPW = 32 / LPR;
@@ -800,7 +801,10 @@ gather_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab dst) {
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
     const int g = lane / LPR, gl = lane % LPR;
-    const int64_t row0 = ((int64_t)blockIdx.x * kWarps + warp) * RPW * GPW;
+    unsigned sent = 0;
+    // grid-stride over passes of RPW row groups per warp (one counter atomic per block)
+    for (int64_t row0 = ((int64_t)blockIdx.x * kWarps + warp) * RPW * GPW; row0 < h.M;
+         row0 += (int64_t)gridDim.x * kWarps * RPW * GPW) {
     float4 xs[RPW][VPL], ss[RPW][VPL];
 #pragma unroll
     for (int r = 0; r < RPW; ++r) {
@@ -819,7 +823,6 @@ gather_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab dst) {
             }
         }
     }
-    unsigned sent = 0;
 #pragma unroll
     for (int r = 0; r < RPW; ++r) {
         const int64_t row = row0 + r * GPW + g;
@@ -850,9 +853,9 @@ gather_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab dst) {
         const int q = find_seg(s_moff, h.p, row);
         uint8_t* slot = dst.base[q] + (row - s_moff[q]) * a.stride;
         float* sr = a.nocache ? nullptr : a.c.s_mir + row * a.ld;
-        if (h.quant) {
-            const QRow qr = qrow(lo, hi, h.quant);
-            const float stp = stepq(lo, hi, h.quant);
+        if constexpr (QB != 0) {
+            const QRow qr = qrow(lo, hi, QB);
+            const float stp = stepq(lo, hi, QB);
             if (gl == 0) st_hdr(slot, a.gstamp, lo, hi);
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
@@ -863,7 +866,7 @@ gather_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab dst) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) dd[k] = __fsub_rn(comp(xs[r][v], k), comp(ss[r][v], k));
                 qx4(dd, qr, qc);
-                store_codes4(slot + 16, c0, a.F, qc, h.quant);
+                store_codes4(slot + 16, c0, a.F, qc, QB);
                 if (sr) {
                     float4 snew;
 #pragma unroll
@@ -887,6 +890,7 @@ gather_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab dst) {
             }
         }
     }
+    }
     if (lane == 0 && sent) atomicAdd(&s_cnt, sent);
     __syncthreads();
     if (threadIdx.x == 0 && s_cnt) atomicAdd(&a.stats[0], (unsigned long long)s_cnt);
@@ -896,13 +900,10 @@ gather_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab dst) {
 // master apply + scatter (Alg. 2 L10-L22): one row group per boundary master row.  Lane s of
 // the group holds the row's slot in the halo list shared with part s (static, -1: no replica
 // on s) — the slot its gather message arrives in and the slot its scatter message goes to.
-template <int LPR, int VPL>
-__global__ void __launch_bounds__(kThreads, VPL <= 2 ? 4 : 1)
-master_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab src, const __grid_constant__ SlotTab sdst) {
-    constexpr int GPW = 32 / LPR;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane / LPR, gl = lane % LPR;
-    const int64_t row = ((int64_t)blockIdx.x * kWarps + warp) * GPW + g;
+template <int LPR, int VPL, int QB>
+__device__ __forceinline__ void master_slot_row(const HaloDev& h, const SyncArgs& a, const SlotTab& src,
+                                                const SlotTab& sdst, int64_t row, int g, int gl,
+                                                unsigned& n_fired, unsigned& n_active, unsigned& n_msgs) {
     const bool valid = row < h.B;
     const int64_t r = valid ? row : 0;
     const int p = h.p;
@@ -951,14 +952,14 @@ master_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab src, c
         }
         any_msg = true;
         const uint8_t* pay = src.base[s] + (int64_t)hps * a.stride + 16;
-        if (h.quant) {
-            const float stp = stepq(lo, hi, h.quant);
+        if constexpr (QB != 0) {
+            const float stp = stepq(lo, hi, QB);
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
                 if (c0 >= a.F) continue;
                 uint32_t qc[4];
-                load_codes4(pay, c0, h.quant, qc);
+                load_codes4(pay, c0, QB, qc);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     if (c0 + k < a.F) setc(acc[v], k, __fadd_rn(comp(acc[v], k), dqv(qc[k], lo, stp)));
@@ -1026,16 +1027,16 @@ master_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab src, c
             if (c0 + k < a.F) { lo = fminf(lo, dk); hi = fmaxf(hi, dk); }
         }
     }
-    if (h.quant) {
+    if constexpr (QB != 0) {
         lo = gmin<LPR>(lo);
         hi = gmax<LPR>(hi);
     }
     int nmsg = 0;
     if (act) {
         uint32_t pk[VPL][2];
-        if (h.quant) {
-            const QRow qr = qrow(lo, hi, h.quant);
-            const float stp = stepq(lo, hi, h.quant);
+        if constexpr (QB != 0) {
+            const QRow qr = qrow(lo, hi, QB);
+            const float stp = stepq(lo, hi, QB);
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
@@ -1047,7 +1048,7 @@ master_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab src, c
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     if (c0 + k < a.F) setc(b[v], k, __fadd_rn(comp(b[v], k), dqv(qc[k], lo, stp)));
-                pack_codes4(qc, c0, a.F, h.quant, pk[v]);
+                pack_codes4(qc, c0, a.F, QB, pk[v]);
             }
         } else {
 #pragma unroll
@@ -1075,11 +1076,11 @@ master_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab src, c
                 uint8_t* slot = sdst.base[s] + (int64_t)hps * a.stride;
                 ++nmsg;
                 if (gl == 0) st_hdr(slot, a.sstamp, lo, hi);
-                if (h.quant) {
+                if constexpr (QB != 0) {
 #pragma unroll
                     for (int v = 0; v < VPL; ++v) {
                         const int c0 = (gl + v * LPR) * 4;
-                        if (c0 < a.F) put_codes4(slot + 16, c0, h.quant, pk[v]);
+                        if (c0 < a.F) put_codes4(slot + 16, c0, QB, pk[v]);
                     }
                 } else {
                     float* prow = reinterpret_cast<float*>(slot + 16);
@@ -1103,21 +1104,47 @@ master_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab src, c
             h.active[r] = act ? 1 : 0;
         }
     }
-    const unsigned bf = __ballot_sync(0xffffffffu, fired && gl == 0);
-    const unsigned ba = __ballot_sync(0xffffffffu, act && gl == 0);
-    int ns = (gl == 0) ? nmsg : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
-    if (lane == 0) {
-        if (bf) atomicAdd(&a.stats[1], (unsigned long long)__popc(bf));
-        if (ba) atomicAdd(&a.stats[2], (unsigned long long)__popc(ba));
-        if (ns) atomicAdd(&a.stats[3], (unsigned long long)ns);
+    if (gl == 0) {
+        n_fired += fired ? 1u : 0u;
+        n_active += act ? 1u : 0u;
+        n_msgs += (unsigned)nmsg;
     }
+}
+
+// Grid-stride over warps of row groups (every lane of a warp runs the same iterations, so the
+// full-warp shuffles stay converged); counters are reduced per block, one atomic each.
+template <int LPR, int VPL, int QB>
+__global__ void __launch_bounds__(kThreads, VPL <= 2 ? 3 : 1)
+master_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab src, const __grid_constant__ SlotTab sdst) {
+    constexpr int GPW = 32 / LPR;
+    __shared__ unsigned s_cnt[3];
+    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / LPR, gl = lane % LPR;
+    unsigned nf = 0, na = 0, nm = 0;
+    const int64_t wstride = (int64_t)gridDim.x * kWarps * GPW;
+    for (int64_t base = ((int64_t)blockIdx.x * kWarps + warp) * GPW; base < h.B; base += wstride)
+        master_slot_row<LPR, VPL, QB>(h, a, src, sdst, base + g, g, gl, nf, na, nm);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        nf += __shfl_xor_sync(0xffffffffu, nf, o);
+        na += __shfl_xor_sync(0xffffffffu, na, o);
+        nm += __shfl_xor_sync(0xffffffffu, nm, o);
+    }
+    if (lane == 0) {
+        if (nf) atomicAdd(&s_cnt[0], nf);
+        if (na) atomicAdd(&s_cnt[1], na);
+        if (nm) atomicAdd(&s_cnt[2], nm);
+    }
+    __syncthreads();
+    if (threadIdx.x < 3 && s_cnt[threadIdx.x])
+        atomicAdd(&a.stats[1 + threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
     if (h.remote) __threadfence_system();
 }
 
 // mirrors receive the scatter: b += deq(q) (or b ← a), Z row ← b
-template <int LPR, int VPL>
+template <int LPR, int VPL, int QB>
 __global__ void __launch_bounds__(kThreads) mirror_slot_kernel(HaloDev h, SyncArgs a,
                                                                const __grid_constant__ SlotTab src) {
     constexpr int GPW = 32 / LPR;
@@ -1139,15 +1166,15 @@ __global__ void __launch_bounds__(kThreads) mirror_slot_kernel(HaloDev h, SyncAr
         b[v] = (bmr && c0 < a.ld) ? ld4(bmr + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     if (hd.x == a.sstamp) {
-        if (h.quant) {
+        if constexpr (QB != 0) {
             const float lo = __uint_as_float(hd.y), hi = __uint_as_float(hd.z);
-            const float stp = stepq(lo, hi, h.quant);
+            const float stp = stepq(lo, hi, QB);
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
                 if (c0 >= a.F) continue;
                 uint32_t qc[4];
-                load_codes4(slot + 16, c0, h.quant, qc);
+                load_codes4(slot + 16, c0, QB, qc);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     if (c0 + k < a.F) setc(b[v], k, __fadd_rn(comp(b[v], k), dqv(qc[k], lo, stp)));
@@ -1289,31 +1316,78 @@ int launch_mirror_apply(const HaloDev& h, const SyncArgs& a, const RegionTab& rt
     return 1;
 }
 
+// the slot kernels are instantiated per message width B (QB): the code packing and the
+// quantiser's branches fold at compile time
+#define CDF_QB(QBV, ...)                                           \
+    do {                                                           \
+        if ((QBV) == 8) { constexpr int QB = 8; __VA_ARGS__; }     \
+        else if ((QBV) == 4) { constexpr int QB = 4; __VA_ARGS__; } \
+        else if ((QBV) == 16) { constexpr int QB = 16; __VA_ARGS__; } \
+        else { constexpr int QB = 0; __VA_ARGS__; }                \
+    } while (0)
+
+template <int QB>
+void gather_slot_q(const HaloDev& h, const SyncArgs& a, const SlotTab& dst, cudaStream_t s, const Shape& sh,
+                   unsigned grid) {
+    if (sh.lpr == 2) gather_slot_kernel<2, 1, 1, QB><<<grid, kThreads, 0, s>>>(h, a, dst);
+    else if (sh.lpr == 4) gather_slot_kernel<4, 1, 1, QB><<<grid, kThreads, 0, s>>>(h, a, dst);
+    else if (sh.lpr == 8 && sh.vpl == 1) gather_slot_kernel<8, 1, 1, QB><<<grid, kThreads, 0, s>>>(h, a, dst);
+    else if (sh.lpr == 8) gather_slot_kernel<8, 2, 2, QB><<<grid, kThreads, 0, s>>>(h, a, dst);
+    else if (sh.vpl == 1) gather_slot_kernel<32, 1, 4, QB><<<grid, kThreads, 0, s>>>(h, a, dst);
+    else if (sh.vpl == 2) gather_slot_kernel<32, 2, 4, QB><<<grid, kThreads, 0, s>>>(h, a, dst);
+    else if (sh.vpl == 4) gather_slot_kernel<32, 4, 2, QB><<<grid, kThreads, 0, s>>>(h, a, dst);
+    else gather_slot_kernel<32, 8, 1, QB><<<grid, kThreads, 0, s>>>(h, a, dst);
+}
+
 int launch_gather_slot(const HaloDev& h, const SyncArgs& a, const SlotTab& dst, cudaStream_t s) {
     if (h.M <= 0) return 0;
     const Shape sh = shape_of(a.ld);
     const int rpw = gather_rpw(sh.lpr, sh.vpl);
     const int64_t rpb = (int64_t)kWarps * (32 / sh.lpr) * rpw;
-    const unsigned grid = (unsigned)((h.M + rpb - 1) / rpb);
-    if (sh.lpr == 2) gather_slot_kernel<2, 1, 1><<<grid, kThreads, 0, s>>>(h, a, dst);
-    else if (sh.lpr == 4) gather_slot_kernel<4, 1, 1><<<grid, kThreads, 0, s>>>(h, a, dst);
-    else if (sh.lpr == 8 && sh.vpl == 1) gather_slot_kernel<8, 1, 1><<<grid, kThreads, 0, s>>>(h, a, dst);
-    else if (sh.lpr == 8) gather_slot_kernel<8, 2, 2><<<grid, kThreads, 0, s>>>(h, a, dst);
-    else if (sh.vpl == 1) gather_slot_kernel<32, 1, 4><<<grid, kThreads, 0, s>>>(h, a, dst);
-    else if (sh.vpl == 2) gather_slot_kernel<32, 2, 4><<<grid, kThreads, 0, s>>>(h, a, dst);
-    else if (sh.vpl == 4) gather_slot_kernel<32, 4, 2><<<grid, kThreads, 0, s>>>(h, a, dst);
-    else gather_slot_kernel<32, 8, 1><<<grid, kThreads, 0, s>>>(h, a, dst);
+    const unsigned grid = (unsigned)std::min<int64_t>((h.M + rpb - 1) / rpb, 148 * 4);
+    CDF_QB(h.quant, gather_slot_q<QB>(h, a, dst, s, sh, grid));
     return 1;
 }
+
+template <int LPR, int VPL>
+struct MasterSlotQ {
+    template <int QB>
+    static void go(unsigned g, cudaStream_t s, const HaloDev& h, const SyncArgs& a, const SlotTab& src,
+                   const SlotTab& sdst) {
+        master_slot_kernel<LPR, VPL, QB><<<g, kThreads, 0, s>>>(h, a, src, sdst);
+    }
+};
+template <int LPR, int VPL>
+struct MirrorSlotQ {
+    template <int QB>
+    static void go(unsigned g, cudaStream_t s, const HaloDev& h, const SyncArgs& a, const SlotTab& src) {
+        mirror_slot_kernel<LPR, VPL, QB><<<g, kThreads, 0, s>>>(h, a, src);
+    }
+};
+// row-width shape x message width dispatch of a slot kernel family F (MasterSlotQ / MirrorSlotQ)
+#define CDF_DISPATCH_SLOT(LD, QBV, F, GRID, STREAM, ...)                                          \
+    do {                                                                                          \
+        Shape _s = shape_of(LD);                                                                  \
+        if (_s.lpr == 2) CDF_QB(QBV, F<2, 1>::template go<QB>(GRID(2), STREAM, __VA_ARGS__));      \
+        else if (_s.lpr == 4) CDF_QB(QBV, F<4, 1>::template go<QB>(GRID(4), STREAM, __VA_ARGS__)); \
+        else if (_s.lpr == 8 && _s.vpl == 1) CDF_QB(QBV, F<8, 1>::template go<QB>(GRID(8), STREAM, __VA_ARGS__)); \
+        else if (_s.lpr == 8) CDF_QB(QBV, F<8, 2>::template go<QB>(GRID(8), STREAM, __VA_ARGS__)); \
+        else if (_s.lpr == 16) CDF_QB(QBV, F<16, 1>::template go<QB>(GRID(16), STREAM, __VA_ARGS__)); \
+        else if (_s.vpl == 1) CDF_QB(QBV, F<32, 1>::template go<QB>(GRID(32), STREAM, __VA_ARGS__)); \
+        else if (_s.vpl == 2) CDF_QB(QBV, F<32, 2>::template go<QB>(GRID(32), STREAM, __VA_ARGS__)); \
+        else if (_s.vpl == 4) CDF_QB(QBV, F<32, 4>::template go<QB>(GRID(32), STREAM, __VA_ARGS__)); \
+        else CDF_QB(QBV, F<32, 8>::template go<QB>(GRID(32), STREAM, __VA_ARGS__));                \
+    } while (0)
 
 int launch_master_slot(const HaloDev& h, const SyncArgs& a, const SlotTab& src, const SlotTab& sdst,
                        cudaStream_t s) {
     if (h.B <= 0) return 0;
+    // grid-stride: 3 resident blocks per SM (148 SMs), fewer for short launches
     auto grid = [&](int lpr) {
         const int64_t rows_per_block = kWarps * (32 / lpr);
-        return (unsigned)((h.B + rows_per_block - 1) / rows_per_block);
+        return (unsigned)std::min<int64_t>((h.B + rows_per_block - 1) / rows_per_block, 148 * 3);
     };
-    CDF_DISPATCH(a.ld, master_slot_kernel, grid, s, h, a, src, sdst);
+    CDF_DISPATCH_SLOT(a.ld, h.quant, MasterSlotQ, grid, s, h, a, src, sdst);
     return 1;
 }
 
@@ -1323,7 +1397,7 @@ int launch_mirror_slot(const HaloDev& h, const SyncArgs& a, const SlotTab& src, 
         const int64_t rows_per_block = kWarps * (32 / lpr);
         return (unsigned)((h.M + rows_per_block - 1) / rows_per_block);
     };
-    CDF_DISPATCH(a.ld, mirror_slot_kernel, grid, s, h, a, src);
+    CDF_DISPATCH_SLOT(a.ld, h.quant, MirrorSlotQ, grid, s, h, a, src);
     return 1;
 }
 
