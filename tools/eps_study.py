@@ -75,6 +75,9 @@ def main():
         print(json.dumps(summary), flush=True)
         results.append({"summary": summary, "epochs": rows})
         run.close()
+        run.workspace = None          # one workspace at a time (C4 p=4 co-resident needs ~96 GB)
+        del run
+        torch.cuda.empty_cache()
     out = a.out or os.path.join(ROOT, "profiles", f"eps_study_{a.config}_p{a.p}_snr{a.snr}.json")
     with open(out, "w") as f:
         json.dump({"source": "tools/eps_study.py", "paper": "Fig. 7 analogue (P:L843-879); "
