@@ -932,8 +932,62 @@ __device__ __forceinline__ void master_slot_row(const HaloDev& h, const SyncArgs
     const unsigned have = (__ballot_sync(0xffffffffu, hp >= 0 && !a.no_msgs && hd.x == a.gstamp) & gmask) >> (g * LPR);
     const unsigned peers = (__ballot_sync(0xffffffffu, hp >= 0) & gmask) >> (g * LPR);
     bool any_msg = false;
-    // Alg. 2 L11-L13: received Δ in ascending source part (R13)
-    for (int s = 0; s < p; ++s) {
+    // The code words of the first NSP sources' slots are loaded together with their headers
+    // (the slot address only needs hpos): one dependent round trip less per message; a stale
+    // slot's words are loaded and ignored.
+    constexpr int NSP = 4, NW = QB == 16 ? 2 : 1;
+    uint32_t pre[NSP][VPL][NW];
+    if constexpr (QB != 0) {
+#pragma unroll
+        for (int s = 0; s < NSP; ++s) {
+            const int32_t hps = __shfl_sync(gmask, hp, g * LPR + (s < LPR ? s : 0));
+            const bool live = lanes_hold && s < p && s != h.me && hps >= 0 && !a.no_msgs;
+            const uint8_t* pay = live ? src.base[s] + (int64_t)hps * a.stride + 16 : nullptr;
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                uint32_t w[2] = {0u, 0u};
+                if (live && c0 < a.F) fetch_codes4(pay, c0, QB, w);
+#pragma unroll
+                for (int t = 0; t < NW; ++t) pre[s][v][t] = w[t];
+            }
+        }
+    }
+    // Alg. 2 L11-L13: received Δ in ascending source part (R13) — first the prefetched sources
+#pragma unroll
+    for (int s = 0; s < NSP; ++s) {
+        if (!lanes_hold || s >= p || s == h.me || !((have >> s) & 1u)) continue;
+        const float lo = __uint_as_float(__shfl_sync(gmask, hd.y, g * LPR + s));
+        const float hi = __uint_as_float(__shfl_sync(gmask, hd.z, g * LPR + s));
+        any_msg = true;
+        if constexpr (QB != 0) {
+            const float stp = stepq(lo, hi, QB);
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 >= a.F) continue;
+                uint32_t w[2] = {pre[s][v][0], NW == 2 ? pre[s][v][NW - 1] : 0u};
+                uint32_t qc[4];
+                unpack_codes4(w, QB, qc);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (c0 + k < a.F) setc(acc[v], k, __fadd_rn(comp(acc[v], k), dqv(qc[k], lo, stp)));
+            }
+        } else {
+            const int32_t hps = __shfl_sync(gmask, hp, g * LPR + s);
+            const float* prow = reinterpret_cast<const float*>(src.base[s] + (int64_t)hps * a.stride + 16);
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c0 = (gl + v * LPR) * 4;
+                if (c0 >= a.ld) continue;
+                const float4 pv = ld4(prow + c0);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) setc(acc[v], k, __fadd_rn(comp(acc[v], k), comp(pv, k)));
+            }
+        }
+    }
+    // ... then the rest (sources >= NSP, or every source when the group's lanes cannot hold p)
+    for (int s = lanes_hold ? NSP : 0; s < p; ++s) {
         if (s == h.me) continue;
         int32_t hps;
         float lo = 0.f, hi = 0.f;
