@@ -986,6 +986,18 @@ int spmm_part(cdfgnn_ctx* c, LocalPart& P, const float* T, float* Y, int64_t ld,
     const int64_t n = rows == 0 ? S.n_items : (rows == 1 ? S.n_items_mir : S.n_items - S.n_items_mir);
     if (n <= 0) return CDFGNN_OK;
     mark(c, PH_SPMM, s, ld);
+    // column slices (CDFGNN_SPMM_CSLICE = slice width): each pass gathers an L2-sized slice of T
+    const int cslice = env_knob("CDFGNN_SPMM_CSLICE", 0);
+    if (cslice > 0 && ld > cslice && rows == 0 && cslice % 4 == 0) {
+        for (int64_t c0 = 0; c0 < ld; c0 += cslice) {
+            const int64_t w = std::min<int64_t>(ld - c0, cslice);
+            const SpmmPlan& Sw = spmm_plan(P, w);
+            if (Sw.nslots && w > Sw.pstride) CDF_FAIL(CDFGNN_EUSAGE, "column slice wider than the split-row scratch");
+            launch_spmm(P.rowptr, P.colidx, P.val, Sw.n_items, spmm_items(P, 0, w), T + c0, Y + c0, ld, s, w);
+            c->launches++;
+        }
+        return check_launch("spmm");
+    }
     launch_spmm(P.rowptr, P.colidx, P.val, n, spmm_items(P, rows, ld), T, Y, ld, s);
     c->launches++;
     return check_launch("spmm");
@@ -1924,8 +1936,8 @@ extern "C" int cdfgnn_spmm(cdfgnn_ctx* c, int32_t lp, const float* T, float* Y, 
     if (S.nslots && ld > S.pstride)
         CDF_FAIL(CDFGNN_EUSAGE, "ld %lld exceeds the split-row scratch stride %lld (widest layer)", (long long)ld,
                  (long long)S.pstride);
-    launch_spmm(P.rowptr, P.colidx, P.val, S.n_items, spmm_items(P, 0, ld), T, Y, ld, (cudaStream_t)stream);
-    return check_launch("spmm");
+    (void)S;
+    return spmm_part(c, P, T, Y, ld, (cudaStream_t)stream, 0);
 }
 
 extern "C" int cdfgnn_bandwidth_probe(const void* buf, int64_t bytes, int32_t reps, double* gbs, void* stream) {

@@ -227,9 +227,9 @@ void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val,
     if (width <= 0) width = ld;
     const int nv = (int)(width / 4);   // float4 per row (width % 4 == 0, width <= 1024)
     const int unr = env_int("CDFGNN_SPMM_UNR", 0);
-    const int tail = env_int("CDFGNN_SPMM_TAIL", ld > 64 ? 1 : 0);   // predicated tail for wide rows
+    const int tail = env_int("CDFGNN_SPMM_TAIL", width > 64 ? 1 : 0);   // predicated tail for wide rows
     // narrow rows: stream the CSR arrays and the output past L2 (evict-first), keeping T's lines
-    const int stream = env_int("CDFGNN_SPMM_STREAM", ld <= 64 ? 1 : 0);
+    const int stream = env_int("CDFGNN_SPMM_STREAM", width <= 64 ? 1 : 0);
     if (nv <= 2) launch<2, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
     else if (nv <= 4) launch<4, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
     else if (nv <= 8) launch<8, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);

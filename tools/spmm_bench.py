@@ -8,7 +8,7 @@ sys.path.insert(0, ROOT)
 
 KNOBS = {"chunk": "CDFGNN_SPMM_CHUNK", "wchunk": "CDFGNN_SPMM_CHUNK_WIDE", "phases": "CDFGNN_SPMM_PHASES", "pmin": "CDFGNN_SPMM_PHASE_MIN", "unr": "CDFGNN_SPMM_UNR", "tail": "CDFGNN_SPMM_TAIL",
          "stream": "CDFGNN_SPMM_STREAM", "shape": "CDFGNN_SPMM_SHAPE", "wshape": "CDFGNN_SPMM_WSHAPE",
-         "order": "CDFGNN_SPMM_ORDER", "heavy": "CDFGNN_SPMM_HEAVY"}
+         "order": "CDFGNN_SPMM_ORDER", "heavy": "CDFGNN_SPMM_HEAVY", "cslice": "CDFGNN_SPMM_CSLICE"}
 
 
 def main():
