@@ -10,6 +10,7 @@ copy torch already loaded.
 """
 import argparse
 import glob
+import hashlib
 import os
 import shutil
 import subprocess
@@ -48,20 +49,34 @@ def _headers():
             + glob.glob(os.path.join(INCLUDE, "*.h")))
 
 
+def _digest(src, cmd):
+    """Content hash of a source, every header it may include and the compile command: an
+    object is reused only when this matches its stamp (mtimes alone can be stale after a
+    checkout or a copy)."""
+    h = hashlib.sha256(" ".join(cmd).encode())
+    for f in [src] + sorted(_headers()):
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
 def _compile(src, nccl_inc, force, verbose):
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-    newest_dep = max([os.path.getmtime(src)] + [os.path.getmtime(h) for h in _headers()])
-    if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest_dep:
-        return obj
+    stamp = obj + ".sha256"
     cmd = [NVCC, "-c", src, "-o", obj, "-O3", "-std=c++17", "-lineinfo", *ARCH,
            "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "-I", INCLUDE, "-I", CSRC, "-I", nccl_inc,
            "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3"]
+    dig = _digest(src, cmd)
+    if not force and os.path.exists(obj) and os.path.exists(stamp) and open(stamp).read() == dig:
+        return obj, False
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
     if verbose and r.stderr:
         print(r.stderr, file=sys.stderr)
-    return obj
+    with open(stamp, "w") as fh:
+        fh.write(dig)
+    return obj, True
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -69,8 +84,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nccl_inc, nccl_lib = _nccl_dirs()
     srcs = _sources()
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, nccl_inc, force, verbose), srcs))
-    if not force and os.path.exists(LIB) and \
+        res = list(ex.map(lambda s: _compile(s, nccl_inc, force, verbose), srcs))
+    objs = [o for o, _ in res]
+    # stale objects of removed sources must not be linked
+    for o in glob.glob(os.path.join(OBJ, "*.o")):
+        if o not in objs:
+            os.remove(o)
+    if not force and not any(rebuilt for _, rebuilt in res) and os.path.exists(LIB) and \
             os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
         return LIB
     tmp = LIB + ".tmp"
