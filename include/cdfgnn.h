@@ -188,6 +188,11 @@ typedef struct {
                                            f32 hi, u32 0} + code row — stamped with the phase's
                                            sequence number; senders store straight into the
                                            receiver's region (through CUDA IPC on a peer GPU) */
+    int32_t fuse_gather;                /* 1 (default): with the slot layout and p > 1 the forward
+                                           SpMM's epilogue runs the gather of its synchronisation
+                                           (Alg. 2 L3-L9: test, quantise, slot store, snapshot) on the
+                                           mirror rows it just computed, from registers (§8 f1);
+                                           0: separate gather kernel.  Bitwise-identical results */
 } cdfgnn_cfg;
 
 int cdfgnn_cfg_default(cdfgnn_cfg* cfg);

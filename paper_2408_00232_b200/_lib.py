@@ -68,7 +68,8 @@ class CfgC(ctypes.Structure):
                 ("eps_clamp", c_i32), ("quant_bits", c_i32), ("optimizer", c_i32), ("lr", c_f64),
                 ("beta1", c_f64), ("beta2", c_f64), ("adam_eps", c_f64), ("gemm_tf32", c_i32),
                 ("timing", c_i32), ("transport", c_i32), ("elide_dead_syncs", c_i32),
-                ("static_inputs", c_i32), ("overlap", c_i32), ("msg_layout", c_i32)]
+                ("static_inputs", c_i32), ("overlap", c_i32), ("msg_layout", c_i32),
+                ("fuse_gather", c_i32)]
 
 
 class MsgViewC(ctypes.Structure):

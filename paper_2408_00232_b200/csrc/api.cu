@@ -981,14 +981,14 @@ int read_stats_now(cdfgnn_ctx* c, int l, int dir, int64_t wire, cudaStream_t s,
 
 // rows: 0 = all rows (longest first), 1 = mirror rows only, 2 = master + interior rows only
 int spmm_part(cdfgnn_ctx* c, LocalPart& P, const float* T, float* Y, int64_t ld, cudaStream_t s,
-              int rows = 0) {
+              int rows = 0, const GatherFuse* gf = nullptr) {
     const SpmmPlan& S = spmm_plan(P, ld);
     const int64_t n = rows == 0 ? S.n_items : (rows == 1 ? S.n_items_mir : S.n_items - S.n_items_mir);
     if (n <= 0) return CDFGNN_OK;
     mark(c, PH_SPMM, s, ld);
     // column slices (CDFGNN_SPMM_CSLICE = slice width): each pass gathers an L2-sized slice of T
     const int cslice = env_knob("CDFGNN_SPMM_CSLICE", 0);
-    if (cslice > 0 && ld > cslice && rows == 0 && cslice % 4 == 0) {
+    if (cslice > 0 && ld > cslice && rows == 0 && cslice % 4 == 0 && !gf) {
         for (int64_t c0 = 0; c0 < ld; c0 += cslice) {
             const int64_t w = std::min<int64_t>(ld - c0, cslice);
             const SpmmPlan& Sw = spmm_plan(P, w);
@@ -998,9 +998,15 @@ int spmm_part(cdfgnn_ctx* c, LocalPart& P, const float* T, float* Y, int64_t ld,
         }
         return check_launch("spmm");
     }
-    launch_spmm(P.rowptr, P.colidx, P.val, n, spmm_items(P, rows, ld), T, Y, ld, s);
+    launch_spmm(P.rowptr, P.colidx, P.val, n, spmm_items(P, rows, ld), T, Y, ld, s, 0, gf);
     c->launches++;
     return check_launch("spmm");
+}
+
+// §8 f1: the forward SpMM runs the gather of its synchronisation in its epilogue (slot layout,
+// no boundary-rows-first split; cfg.fuse_gather = 0 disables it)
+bool fuse_gather_on(const cdfgnn_ctx* c) {
+    return c->cfg.fuse_gather != 0 && c->slot && c->p > 1;
 }
 
 // cfg.static_inputs == 2 (hoisted input aggregation): X is fixed per buffer, so the
@@ -1056,6 +1062,13 @@ int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, cons
         mark(c, PH_GEMM, s);
         c->launches += launch_transpose(W, Fi, Fo, Fo, Wt, ldwt, s);
     }
+    const bool fuse = !ov && !hz && fuse_gather_on(c) && env_knob("CDFGNN_SPMM_CSLICE", 0) == 0;
+    std::vector<SyncArgs> fargs;
+    if (fuse) {
+        if (ld_out != ld_of(Fo)) CDF_FAIL(CDFGNN_EUSAGE, "ld %lld must equal roundup(F, 4)", (long long)ld_out);
+        new_stamps(c, l, 0, ld_out);
+        sync_args(c, l, 0, Z, ld_out, eps, false, fargs);
+    }
     for (int t = 0; t < c->k; ++t) {
         LocalPart& P = c->parts[t];
         const float* A = H_in[t];
@@ -1073,9 +1086,30 @@ int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, cons
         }
         c->launches++;
         CDF_TRY(check_launch("gemm fwd"));
-        if (!hz) CDF_TRY(spmm_part(c, P, P.T, Z[t], ld_out, s, ov ? 1 : 0));
+        if (fuse) {
+            GatherFuse gf;
+            gf.h = halo_for(c, P, l, 0);
+            gf.a = fargs[t];
+            gf.dst = P.gdst;
+            CDF_TRY(spmm_part(c, P, P.T, Z[t], ld_out, s, 0, &gf));
+        } else if (!hz) {
+            CDF_TRY(spmm_part(c, P, P.T, Z[t], ld_out, s, ov ? 1 : 0));
+        }
     }
-    if (ov) {
+    if (fuse) {
+        // the gather ran in the SpMM epilogues: count its senders, transfer barrier, then the
+        // master apply and scatter (Alg. 2 L10-L22)
+        mark(c, PH_SYNC, s, SS_GPACK);
+        for (int t = 0; t < c->k; ++t) {
+            LocalPart& P = c->parts[t];
+            launch_count_flags(halo_for(c, P, l, 0).gflag, P.M, fargs[t].stats, s);
+            c->launches++;
+        }
+        CDF_TRY(check_launch("count_flags"));
+        mark(c, PH_SYNC, s, SS_GXFER);
+        if (c->transport == 2) CDF_TRY(push_barrier(c, s));
+        CDF_TRY(halo_finish(c, l, 0, Z, ld_out, eps, s, wire, false, elide && l == c->cfg.L));
+    } else if (ov) {
         // §8 f1: the mirror rows are done — their gather runs on s2 under the remaining SpMM rows
         CDF_TRY(launch_gather_async(c, l, 0, Z, ld_out, eps, s, wire));
         for (int t = 0; t < c->k; ++t) CDF_TRY(spmm_part(c, c->parts[t], c->parts[t].T, Z[t], ld_out, s, 2));
@@ -1233,6 +1267,7 @@ extern "C" int cdfgnn_cfg_default(cdfgnn_cfg* cfg) {
     cfg->static_inputs = 0;
     cfg->overlap = 0;
     cfg->msg_layout = 0;
+    cfg->fuse_gather = 1;
     return CDFGNN_OK;
 }
 

@@ -147,10 +147,21 @@ struct SpmmItems {
 int spmm_chunk(bool wide, int64_t nnz);
 int spmm_default_phases();
 int spmm_phase_min_degree();
+// SpMM epilogue fused with the gather of the following synchronisation (§8 f1): a row group that
+// finished a mirror row [B, B+M) runs Alg. 2 L3-L9 on it from registers (test, quantise, slot
+// store, snapshot, flag) — the separate gather kernel's re-read of Z disappears.
+struct GatherFuse {
+    HaloDev h;
+    SyncArgs a;
+    SlotTab dst;
+};
 // width (<= 1024, % 4 == 0; default ld): the columns computed; ld: row stride of T and Y.  Split-row
-// partials are width floats per slot.
+// partials are width floats per slot.  gf (optional): fuse the gather into the epilogue.
 void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val, int64_t n_items,
-                 const SpmmItems& it, const float* T, float* Y, int64_t ld, cudaStream_t s, int64_t width = 0);
+                 const SpmmItems& it, const float* T, float* Y, int64_t ld, cudaStream_t s, int64_t width = 0,
+                 const GatherFuse* gf = nullptr);
+// stats[0] += number of set flags (uint8) among n (the fused gather's sent count)
+void launch_count_flags(const uint8_t* f, int64_t n, unsigned long long* out, cudaStream_t s);
 
 // ---- dense (kernels_dense.cu)
 // C[M x ldc] = op(A) op(B) (+ mask) ; columns [N, ldc) of C are written as zero.

@@ -26,13 +26,16 @@ namespace {
 
 constexpr int kThreads = 256;
 
-template <int LPR, int VPL, int UNR, int TAIL>
+#include "halo_common.cuh"
+
+template <int LPR, int VPL, int UNR, int TAIL, bool FUSE>
 __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n_items, const int32_t* __restrict__ rowptr,
                                                         const int32_t* __restrict__ colidx,
                                                         const float* __restrict__ val,
                                                         const float* __restrict__ T,
                                                         float* __restrict__ Y, int64_t ld, int64_t width,
-                                                        SpmmItems it, int stream) {
+                                                        SpmmItems it, int stream,
+                                                        const __grid_constant__ GatherFuse gf) {
     constexpr int GPW = 32 / LPR;
     const int lane = threadIdx.x & 31;
     const int g = lane / LPR, gl = lane % LPR;
@@ -187,17 +190,50 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n_items, const i
             float4* yp = reinterpret_cast<float4*>(yr + (gl + v * LPR) * 4);
             if (stream) __stcs(yp, acc[v]); else *yp = acc[v];
         }
+    if constexpr (FUSE) {
+        // a mirror row: the following synchronisation's gather (Alg. 2 L3-L9) from registers
+        const int64_t mrow = row - gf.h.B;
+        if (mrow >= 0 && mrow < gf.h.M) {
+            const int q = find_seg(gf.h.moff, gf.h.p, mrow);
+            uint8_t* slot = gf.dst.base[q] + (mrow - gf.h.moff[q]) * gf.a.stride;
+            gather_row_fused<LPR, VPL>(gf.h, gf.a, slot, mrow, gmask, gl, acc);
+        }
+    }
+}
+
+__global__ void count_flags_kernel(const uint8_t* __restrict__ f, int64_t n, unsigned long long* out) {
+    unsigned c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        c += f[i] ? 1u : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    __shared__ unsigned sc;
+    if (threadIdx.x == 0) sc = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&sc, c);
+    __syncthreads();
+    if (threadIdx.x == 0 && sc) atomicAdd(out, (unsigned long long)sc);
 }
 
 template <int LPR, int VPL, int UNR>
 void launch(int64_t n, const int32_t* rowptr, const int32_t* colidx, const float* val, const float* T, float* Y,
-            int64_t ld, int64_t width, const SpmmItems& it, cudaStream_t s, int tail, int stream) {
+            int64_t ld, int64_t width, const SpmmItems& it, cudaStream_t s, int tail, int stream,
+            const GatherFuse* gf) {
     const int64_t rows_per_block = (kThreads / 32) * (32 / LPR);
     const unsigned grid = (unsigned)((n + rows_per_block - 1) / rows_per_block);
-    if (tail)
-        spmm_kernel<LPR, VPL, UNR, 1><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream);
-    else
-        spmm_kernel<LPR, VPL, UNR, 0><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream);
+    static const GatherFuse none{};
+    const GatherFuse& g = gf ? *gf : none;
+    if (gf) {
+        if (tail)
+            spmm_kernel<LPR, VPL, UNR, 1, true><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream, g);
+        else
+            spmm_kernel<LPR, VPL, UNR, 0, true><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream, g);
+    } else {
+        if (tail)
+            spmm_kernel<LPR, VPL, UNR, 1, false><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream, g);
+        else
+            spmm_kernel<LPR, VPL, UNR, 0, false><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream, g);
+    }
 }
 
 int env_int(const char* name, int dflt) {
@@ -221,8 +257,14 @@ int spmm_chunk(bool wide, int64_t nnz) {
 int spmm_default_phases() { return env_int("CDFGNN_SPMM_PHASES", 1); }
 int spmm_phase_min_degree() { return env_int("CDFGNN_SPMM_PHASE_MIN", 64); }
 
+void launch_count_flags(const uint8_t* f, int64_t n, unsigned long long* out, cudaStream_t s) {
+    if (n <= 0) return;
+    count_flags_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4), 256, 0, s>>>(f, n, out);
+}
+
 void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val, int64_t n_items,
-                 const SpmmItems& it, const float* T, float* Y, int64_t ld, cudaStream_t s, int64_t width) {
+                 const SpmmItems& it, const float* T, float* Y, int64_t ld, cudaStream_t s, int64_t width,
+                 const GatherFuse* gf) {
     if (n_items <= 0) return;
     if (width <= 0) width = ld;
     const int nv = (int)(width / 4);   // float4 per row (width % 4 == 0, width <= 1024)
@@ -230,35 +272,35 @@ void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val,
     const int tail = env_int("CDFGNN_SPMM_TAIL", width > 64 ? 1 : 0);   // predicated tail for wide rows
     // narrow rows: stream the CSR arrays and the output past L2 (evict-first), keeping T's lines
     const int stream = env_int("CDFGNN_SPMM_STREAM", width <= 64 ? 1 : 0);
-    if (nv <= 2) launch<2, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
-    else if (nv <= 4) launch<4, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
-    else if (nv <= 8) launch<8, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+    if (nv <= 2) launch<2, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+    else if (nv <= 4) launch<4, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+    else if (nv <= 8) launch<8, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
     else if (nv <= 16) {
         // 8 lanes x 2 float4 per row, 8 neighbours in flight, predicated tail batch: at ld = 44
         // (C3's 41 classes) 1.75 -> 1.48 ms per launch vs 16 lanes x 1 (p = 1, tools/spmm_bench.py,
         // profiles/r1); 4x3 and 2x6 were slower (fewer neighbours in flight per lane)
         const int shape = env_int("CDFGNN_SPMM_SHAPE", 3);
-        if (shape == 1 && nv <= 12) launch<4, 3, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream);
-        else if (shape == 2 && nv <= 12) launch<2, 6, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream);
-        else if (shape == 3) launch<8, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream);
-        else if (shape == 4) launch<16, 1, 16>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream);
-        else if (shape == 5) launch<4, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream);
-        else if (shape == 6) launch<8, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream);
-        else if (unr == 4) launch<16, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
-        else launch<16, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+        if (shape == 1 && nv <= 12) launch<4, 3, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf);
+        else if (shape == 2 && nv <= 12) launch<2, 6, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf);
+        else if (shape == 3) launch<8, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf);
+        else if (shape == 4) launch<16, 1, 16>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf);
+        else if (shape == 5) launch<4, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf);
+        else if (shape == 6) launch<8, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf);
+        else if (unr == 4) launch<16, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+        else launch<16, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
     } else if (nv <= 32) {
-        if (unr == 4) launch<32, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
-        else launch<32, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+        if (unr == 4) launch<32, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+        else launch<32, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
     } else if (nv <= 64) {
         const int wshape = env_int("CDFGNN_SPMM_WSHAPE", 0);
-        if (wshape == 1) launch<16, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
-        else if (wshape == 2) launch<16, 4, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
-        else if (wshape == 3) launch<32, 2, 6>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
-        else if (unr == 2) launch<32, 2, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
-        else if (unr == 8) launch<32, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
-        else launch<32, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
-    } else if (nv <= 128) launch<32, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
-    else launch<32, 8, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream);
+        if (wshape == 1) launch<16, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+        else if (wshape == 2) launch<16, 4, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+        else if (wshape == 3) launch<32, 2, 6>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+        else if (unr == 2) launch<32, 2, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+        else if (unr == 8) launch<32, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+        else launch<32, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+    } else if (nv <= 128) launch<32, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+    else launch<32, 8, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
 }
 
 }  // namespace cdfgnn

@@ -33,7 +33,8 @@ class Run:
                  timing: bool = False, plan: Optional[api.Plan] = None,
                  host_inputs: bool = False, partition_kw: Optional[Dict] = None,
                  gemm: str = "tf32x3", transport: str = "push", elide: bool = True,
-                 static_inputs: int = 0, overlap: bool = False, msg_layout: int = 0):
+                 static_inputs: int = 0, overlap: bool = False, msg_layout: int = 0,
+                 fuse_gather: bool = True):
         import torch
         self.torch = torch
         self.ds = ds
@@ -48,7 +49,8 @@ class Run:
                                    timing=int(timing), gemm_tf32=GEMM_MODES[gemm],
                                    transport={"push": 0, "nccl": 1}[transport],
                                    elide_dead_syncs=int(elide), static_inputs=int(static_inputs),
-                                   overlap=int(overlap), msg_layout=int(msg_layout))
+                                   overlap=int(overlap), msg_layout=int(msg_layout),
+                                   fuse_gather=int(fuse_gather))
         nbytes = api.workspace_size(self.plan, self.parts, self.cfg)
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         uid = None

@@ -197,14 +197,16 @@ def test_label_out_of_range_is_edata():
                                               (True, 8, (20, 24, 16, 6)), (True, 0, (20, 24, 16, 6))])
 def test_dead_sync_elision_static_inputs_and_overlap_are_bitwise_neutral(cache, quant, dims):
     """§8 f2: skipping the layer-L forward scatter and backward gather, and reusing Xᵀ;
-    §8 f1: boundary-rows-first scheduling with the gather on a second stream; the compacted
-    vs slot-addressed message layout — none of them changes a bit of the trajectory."""
+    §8 f1: boundary-rows-first scheduling with the gather on a second stream, and the gather
+    fused into the forward SpMM epilogue; the compacted vs slot-addressed message layout — none
+    of them changes a bit of the trajectory."""
     torch = require_gpu()
     d = small_random_graph(1200, 8000, dims, seed=65)
     runs = [Run(d, 3, cache=cache, quant_bits=quant, eps0=0.01, elide=e, static_inputs=si, overlap=ov,
-                msg_layout=ml)
-            for e, si, ov, ml in ((False, False, False, 0), (True, True, False, 0), (True, True, True, 0),
-                                  (True, True, False, 1), (False, False, False, 1))]
+                msg_layout=ml, fuse_gather=fg)
+            for e, si, ov, ml, fg in ((False, False, False, 0, False), (True, True, False, 0, True),
+                                      (True, True, True, 0, True), (True, True, False, 1, True),
+                                      (False, False, False, 1, True), (True, False, False, 0, False))]
     for ep in range(4):
         res = [r.epoch() for r in runs]
         for r in res[1:]:
