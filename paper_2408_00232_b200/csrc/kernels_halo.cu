@@ -665,91 +665,91 @@ gather_slot_kernel(HaloDev h, SyncArgs a, const __grid_constant__ SlotTab dst) {
     // grid-stride over passes of RPW row groups per warp (one counter atomic per block)
     for (int64_t row0 = ((int64_t)blockIdx.x * kWarps + warp) * RPW * GPW; row0 < h.M;
          row0 += (int64_t)gridDim.x * kWarps * RPW * GPW) {
-    float4 xs[RPW][VPL], ss[RPW][VPL];
+        float4 xs[RPW][VPL], ss[RPW][VPL];
 #pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-        const int64_t row = row0 + r * GPW + g;
-        const bool valid = row < h.M;
-        const float* xr = a.X + (h.B + (valid ? row : 0)) * a.ld;
-        const float* sr = a.nocache ? nullptr : a.c.s_mir + (valid ? row : 0) * a.ld;
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-            const int c0 = (gl + v * LPR) * 4;
-            xs[r][v] = make_float4(0.f, 0.f, 0.f, 0.f);
-            ss[r][v] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (valid && c0 < a.ld) {
-                xs[r][v] = __ldcs(reinterpret_cast<const float4*>(xr + c0));   // read once
-                if (sr) ss[r][v] = __ldcs(reinterpret_cast<const float4*>(sr + c0));
-            }
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-        const int64_t row = row0 + r * GPW + g;
-        const bool valid = row < h.M;
-        float maxs = 0.f, lo = INFINITY, hi = -INFINITY;
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-            const int c0 = (gl + v * LPR) * 4;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float dk = __fsub_rn(comp(xs[r][v], k), comp(ss[r][v], k));
-                if (c0 + k < a.F) {
-                    maxs = fmaxf(maxs, fabsf(comp(ss[r][v], k)));
-                    lo = fminf(lo, dk);
-                    hi = fmaxf(hi, dk);
-                }
-            }
-        }
-        maxs = gmax<LPR>(maxs);
-        lo = gmin<LPR>(lo);
-        hi = gmax<LPR>(hi);
-        // ‖d‖∞ = max(|min d|, |max d|): exact; the test of Alg. 2 L4 (reading R15)
-        const float maxd = valid ? fmaxf(fabsf(lo), fabsf(hi)) : 0.f;
-        const bool flag = valid && (a.nocache || maxd > __fmul_rn(a.eps, maxs));
-        sent += __popc(__ballot_sync(0xffffffffu, flag && gl == 0));
-        if (valid && gl == 0) h.gflag[row] = flag ? 1 : 0;
-        if (!flag) continue;
-        const int q = find_seg(s_moff, h.p, row);
-        uint8_t* slot = dst.base[q] + (row - s_moff[q]) * a.stride;
-        float* sr = a.nocache ? nullptr : a.c.s_mir + row * a.ld;
-        if constexpr (QB != 0) {
-            const QRow qr = qrow(lo, hi, QB);
-            const float stp = stepq(lo, hi, QB);
-            if (gl == 0) st_hdr(slot, a.gstamp, lo, hi);
+        for (int r = 0; r < RPW; ++r) {
+            const int64_t row = row0 + r * GPW + g;
+            const bool valid = row < h.M;
+            const float* xr = a.X + (h.B + (valid ? row : 0)) * a.ld;
+            const float* sr = a.nocache ? nullptr : a.c.s_mir + (valid ? row : 0) * a.ld;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
-                if (c0 >= a.F) continue;
-                uint32_t qc[4];
-                float dd[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) dd[k] = __fsub_rn(comp(xs[r][v], k), comp(ss[r][v], k));
-                qx4(dd, qr, qc);
-                store_codes4(slot + 16, c0, a.F, qc, QB);
-                if (sr) {
-                    float4 snew;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        setc(snew, k, (c0 + k < a.F) ? __fadd_rn(comp(ss[r][v], k), dqv(qc[k], lo, stp)) : 0.f);
-                    __stcs(reinterpret_cast<float4*>(sr + c0), snew);   // reading R11: s ← s + deq(q(Δ))
+                xs[r][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+                ss[r][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (valid && c0 < a.ld) {
+                    xs[r][v] = __ldcs(reinterpret_cast<const float4*>(xr + c0));   // read once
+                    if (sr) ss[r][v] = __ldcs(reinterpret_cast<const float4*>(sr + c0));
                 }
             }
-        } else {
-            if (gl == 0) st_hdr(slot, a.gstamp, 0.f, 0.f);
-            float* prow = reinterpret_cast<float*>(slot + 16);
+        }
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+            const int64_t row = row0 + r * GPW + g;
+            const bool valid = row < h.M;
+            float maxs = 0.f, lo = INFINITY, hi = -INFINITY;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int c0 = (gl + v * LPR) * 4;
-                if (c0 >= a.ld) continue;
-                float4 dv;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) setc(dv, k, __fsub_rn(comp(xs[r][v], k), comp(ss[r][v], k)));
-                st4(prow + c0, dv);
-                if (sr) st4(sr + c0, xs[r][v]);   // Alg. 2 L6: s ← z
+                for (int k = 0; k < 4; ++k) {
+                    const float dk = __fsub_rn(comp(xs[r][v], k), comp(ss[r][v], k));
+                    if (c0 + k < a.F) {
+                        maxs = fmaxf(maxs, fabsf(comp(ss[r][v], k)));
+                        lo = fminf(lo, dk);
+                        hi = fmaxf(hi, dk);
+                    }
+                }
+            }
+            maxs = gmax<LPR>(maxs);
+            lo = gmin<LPR>(lo);
+            hi = gmax<LPR>(hi);
+            // ‖d‖∞ = max(|min d|, |max d|): exact; the test of Alg. 2 L4 (reading R15)
+            const float maxd = valid ? fmaxf(fabsf(lo), fabsf(hi)) : 0.f;
+            const bool flag = valid && (a.nocache || maxd > __fmul_rn(a.eps, maxs));
+            sent += __popc(__ballot_sync(0xffffffffu, flag && gl == 0));
+            if (valid && gl == 0) h.gflag[row] = flag ? 1 : 0;
+            if (!flag) continue;
+            const int q = find_seg(s_moff, h.p, row);
+            uint8_t* slot = dst.base[q] + (row - s_moff[q]) * a.stride;
+            float* sr = a.nocache ? nullptr : a.c.s_mir + row * a.ld;
+            if constexpr (QB != 0) {
+                const QRow qr = qrow(lo, hi, QB);
+                const float stp = stepq(lo, hi, QB);
+                if (gl == 0) st_hdr(slot, a.gstamp, lo, hi);
+#pragma unroll
+                for (int v = 0; v < VPL; ++v) {
+                    const int c0 = (gl + v * LPR) * 4;
+                    if (c0 >= a.F) continue;
+                    uint32_t qc[4];
+                    float dd[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) dd[k] = __fsub_rn(comp(xs[r][v], k), comp(ss[r][v], k));
+                    qx4(dd, qr, qc);
+                    store_codes4(slot + 16, c0, a.F, qc, QB);
+                    if (sr) {
+                        float4 snew;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            setc(snew, k, (c0 + k < a.F) ? __fadd_rn(comp(ss[r][v], k), dqv(qc[k], lo, stp)) : 0.f);
+                        __stcs(reinterpret_cast<float4*>(sr + c0), snew);   // reading R11: s ← s + deq(q(Δ))
+                    }
+                }
+            } else {
+                if (gl == 0) st_hdr(slot, a.gstamp, 0.f, 0.f);
+                float* prow = reinterpret_cast<float*>(slot + 16);
+#pragma unroll
+                for (int v = 0; v < VPL; ++v) {
+                    const int c0 = (gl + v * LPR) * 4;
+                    if (c0 >= a.ld) continue;
+                    float4 dv;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) setc(dv, k, __fsub_rn(comp(xs[r][v], k), comp(ss[r][v], k)));
+                    st4(prow + c0, dv);
+                    if (sr) st4(sr + c0, xs[r][v]);   // Alg. 2 L6: s ← z
+                }
             }
         }
-    }
     }
     if (lane == 0 && sent) atomicAdd(&s_cnt, sent);
     __syncthreads();
