@@ -243,20 +243,21 @@ def remote_split(st, M, L, elide=True):
             "avoided_frac_elision": round(elided / base, 4) if base else None}
 
 
-def halo_bytes(st, dims, M, B, quant, cache=True, elide=True):
+def halo_bytes(st, dims, M, B, quant, cache=True, elide=True, fused=True):
     """Algorithmic HBM bytes of the three halo kernels in one epoch, summed over
     the executed syncs: gather (a3+a4: read z, s of every mirror row = 8F; per sender the
     snapshot write 4F and the message), master (a6+a7: read a, z, s, b = 16F and the received
     messages; write the Z row 4F, a and b 8F per active master, s 4F per fired master, the
     scatter messages), mirror (read b 4F + the message per received row; write b 4F per message,
-    the Z row 4F)."""
+    the Z row 4F).  fused: the forward syncs' gathers run inside the SpMM epilogue
+    (cfg.fuse_gather), so only the backward gathers are attributed to the gather phase."""
     L = len(dims) - 1
     g = m = r = 0
     for d, l, gran, sran in sync_schedule(L, elide):
         s = st[d][l - 1]
         F = dims[l]
         mb = msg_bytes(F, quant)
-        if gran:
+        if gran and not (fused and d == "fwd"):
             g += (8 if cache else 4) * F * M + s["gather_sent"] * ((4 * F if cache else 0) + mb)
         m += (16 if cache else 4) * F * B + s["gather_sent"] * mb + 4 * F * B
         m += (s["active"] * 8 * F + s["master_fired"] * 4 * F if cache else 0) + s["scatter_msgs"] * mb
@@ -424,7 +425,8 @@ def _main(args, real_stdout):
                                                 [round(x, 3) for x in sub]))},
             "halo_kernels": kern,
             "bytes_model": "SURVEY 8(d3) algorithmic bytes of the executed syncs (bench.halo_bytes) / "
-                           "CUDA-event phase time / MEASURED_PEAKS hbm_gbs",
+                           "CUDA-event phase time / MEASURED_PEAKS hbm_gbs; the forward gathers run in "
+                           "the SpMM epilogue (cfg.fuse_gather), so 'gather' covers the backward ones",
             "comm_bytes_per_epoch": int(sum(sum(s["bytes_alg"] for s in x["fwd"] + x["bwd"]) for x in st3)
                                         / args.steps),
             "remote_accesses": {kk: (round(sum(r[kk] for r in rs3) / args.steps)
