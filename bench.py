@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--transport", default="push", choices=["push", "nccl"])
     ap.add_argument("--overlap", action="store_true",
                     help="boundary-rows-first scheduling (gather phase on a second stream; off by default)")
+    ap.add_argument("--fuse", type=int, default=1,
+                    help="cfg.fuse_gather: run each forward sync's gather in the SpMM epilogue (bitwise identical)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--hoisted", type=int, default=1,
                     help="1: also time the hoisted-input-aggregation schedule (static_inputs = 2) and "
@@ -289,7 +291,8 @@ def _main(args, real_stdout):
     cache_on, quant = {"cache_int8": (True, 8), "cache_fp32": (True, 0), "quant_only": (False, 8),
                        "nocache": (False, 0)}[args.mode]
     common = dict(cache=cache_on, quant_bits=quant, eps0=args.eps0, adaptive=True, optimizer="adam",
-                  lr=0.01, timing=True, transport=args.transport, overlap=args.overlap)
+                  lr=0.01, timing=True, transport=args.transport, overlap=args.overlap,
+                  fuse_gather=bool(args.fuse))
     run = Run(ds, world, rank=rank, world=world, device=local, host_inputs=not args.no_e2e,
               static_inputs=True, **common)
     t_prep = time.time() - t_prep
@@ -401,7 +404,7 @@ def _main(args, real_stdout):
         c_ms, st3, _ = timed(lambda i=0: run3.epoch())
         Mk = sum(v["n_mirror"] for v in run3.views)
         Bk = sum(v["n_bmaster"] for v in run3.views)
-        hb = [halo_bytes(x, ds.dims, Mk, Bk, quant, cache_on) for x in st3]
+        hb = [halo_bytes(x, ds.dims, Mk, Bk, quant, cache_on, fused=bool(args.fuse)) for x in st3]
         sub = [sum(x["ms_sync_sub"][i] for x in st3) / args.steps for i in range(6)]
         names = ("gather", "master", "mirror")
         ms_of = {"gather": sub[0], "master": sub[2] + sub[3], "mirror": sub[5]}
