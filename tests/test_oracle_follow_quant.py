@@ -217,3 +217,57 @@ def test_recorded_scatter_codes_rebuild_the_views_fp32():
                               _vertex_of_scatter(plan, j, i, pos))
         nrec += len(pos)
     assert nrec == c.scatter_msgs
+
+
+@pytest.mark.parametrize("eps", [0.0, 0.05, 0.3])
+@pytest.mark.parametrize("B,dt", [(8, np.float64), (0, np.float64), (8, np.float32), (16, np.float64)])
+def test_full_staleness_bound_every_sync(eps, B, dt):
+    """P-C4 in full (Lemma-2 style), vertex by vertex after every sync of a drifting
+    run: ‖b_u − Σ_i z_{i,u}‖∞ ≤ Σ_mirrors e_i + e_master + e_scat, with e = ε‖s‖∞ for a replica
+    that did not send / fire, (hi − lo)/2^B for a quantised mirror sender, 0 for an fp32 sender
+    or a fired master (its own Δ never travels, R13), and e_scat = (hi − lo)/2^B of u's most
+    recent scatter delta (0 without quantisation, R12)."""
+    import copy
+    plan = _plan(3, seed=91)
+    rng = np.random.default_rng(int(eps * 100) + B)
+    F = 6
+    st = SyncState(plan, F, dt)
+    X = [rng.standard_normal((pp.n_local, F)).astype(dt) for pp in plan.parts]
+    e_scat = np.zeros(plan.n)
+    for it in range(10):
+        pre = copy.deepcopy(st)
+        out, c = sync(plan, st, [x.copy() for x in X], eps, SyncMode(cache=True, quant_bits=B, dtype=dt))
+        tot = _exact(plan, X)
+        bound = np.zeros(plan.n)
+        mag = np.zeros(plan.n)
+        for i, pp in enumerate(plan.parts):
+            Bi, Mi = pp.n_bmaster, pp.n_mirror
+            g_m = pp.local2global[Bi:Bi + Mi]
+            s_pre = pre.s_mir[i].astype(np.float64)
+            sent = c.gather_mask[i]
+            e = eps * np.abs(s_pre).max(axis=1) if Mi else np.zeros(0)
+            if B:
+                for (src, dst), (pos, q, lo, hi) in c.gather_msgs.items():
+                    if src == i:
+                        rows = pp.mirror_off[dst] + pos
+                        e[rows] = (hi.astype(np.float64) - lo) / 2.0 ** B
+            else:
+                e[sent] = 0.0
+            np.add.at(bound, g_m, e)
+            g_b = pp.local2global[:Bi]
+            em = eps * np.abs(pre.s_mas[i].astype(np.float64)).max(axis=1) if Bi else np.zeros(0)
+            em[c.master_fired_mask[i]] = 0.0
+            np.add.at(bound, g_b, em)
+            np.maximum.at(mag, pp.local2global, np.abs(X[i].astype(np.float64)).max(axis=1))
+        if B:
+            for (j, i), (pos, q, lo, hi) in c.scatter_msgs_rec.items():
+                e_scat[_vertex_of_scatter(plan, j, i, pos)] = (hi.astype(np.float64) - lo) / 2.0 ** B
+        slack = 1e-12 if dt == np.float64 else 64 * np.finfo(np.float32).eps
+        for pp, o in zip(plan.parts, out):
+            rows = _boundary_rows(pp)
+            g = pp.local2global[rows]
+            err = np.abs(o[rows].astype(np.float64) - tot[g]).max(axis=1)
+            lim = bound[g] + e_scat[g] + slack * (1 + mag[g] * 4)
+            assert (err <= lim * (1 + 1e-9)).all(), (it, float((err - lim).max()))
+        X = _drift(rng, X)
+        X = [x.astype(dt) for x in X]
