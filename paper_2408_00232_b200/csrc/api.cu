@@ -483,7 +483,8 @@ void carve(cdfgnn_ctx* c, Bump& b) {
 
 // ---- phase timing ----------------------------------------------------------------
 void mark(cdfgnn_ctx* c, int phase, cudaStream_t s, int64_t tag = 0) {
-    if (!c->timing) return;
+    // phase times are reported per cdfgnn_epoch (the event list restarts with every epoch)
+    if (!c->timing || !c->in_epoch) return;
     if (c->ev_used >= c->ev.size()) {
         cudaEvent_t e;
         if (cudaEventCreate(&e) != cudaSuccess) return;
