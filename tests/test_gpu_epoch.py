@@ -293,3 +293,52 @@ def test_static_inputs_follow_new_host_inputs():
             x.copy_(x0)
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("name,scale,p", [("C4", 0.01, 4), ("C5", 0.005, 4)])
+def test_C4_C5_shapes_exact_mode(name, scale, p):
+    """The 3-layer C4 (100-256-256-47) and C5 (200-256-256-172) architectures on scaled-down
+    graphs of their degree laws: ε = 0 and fp32 messages (P-C1) — per-epoch loss within 1e-5
+    and W row-normwise within 1e-4 of the oracle (SGD, 4 epochs)."""
+    require_gpu()
+    d = make_dataset(get_config(name), scale)
+    kw = dict(cache=True, quant_bits=0, eps0=0.0, adaptive=False, optimizer="sgd", lr=0.5)
+    run = Run(d, p, **kw)
+    orc = _oracle(d, p, **kw)
+    for ep in range(4):
+        g = run.epoch()
+        o = orc.epoch()
+        assert abs(g["loss"] - o["loss"]) <= 1e-5 * max(1.0, abs(o["loss"])), (ep, g["loss"], o["loss"])
+        for wg, wo in zip(run.weights(), orc.W):
+            assert rownorm_err(wg, wo) <= 1e-4
+    run.close()
+
+
+@pytest.mark.parametrize("name,scale,eps", [("C4", 0.01, 0.03), ("C4", 0.01, 0.1), ("C5", 0.005, 0.1),
+                                            ("C3", 0.02, 0.3)])
+def test_fixed_eps_sweep_follow_mode(name, scale, eps):
+    """Points of the ε sweep (BASELINE configs[3]; §8 f3) with the cache and int8 messages: the
+    oracle follows the GPU's send / fire decisions; per-epoch loss within 1e-3·max(1, |L|) and
+    every sync's counts equal over 15 epochs (SGD), and the cache really skips replicas."""
+    require_gpu()
+    d = make_dataset(get_config(name), scale)
+    kw = dict(cache=True, quant_bits=8, eps0=eps, adaptive=False, optimizer="sgd", lr=0.5)
+    run = Run(d, 4, **kw)
+    orc = _oracle(d, 4, **kw)
+    skipped = 0
+    for ep in range(15):
+        g = run.epoch()
+        o = orc.epoch(follow=gpu_follow_masks(run))
+        assert abs(g["loss"] - o["loss"]) <= 1e-3 * max(1.0, abs(o["loss"])), (ep, g["loss"], o["loss"])
+        oc = {(dr, l): c for dr, l, c in o["counters"]}
+        for l in range(1, run.cfg.L + 1):
+            for dr, key in ((g["fwd"], "fwd"), (g["bwd"], "bwd")):
+                c = oc[(key, l)]
+                assert dr[l - 1]["gather_sent"] == c.gather_sent
+                assert dr[l - 1]["master_fired"] == c.master_fired
+                if not (key == "fwd" and l == run.cfg.L):
+                    assert dr[l - 1]["scatter_msgs"] == c.scatter_msgs
+        M = sum(v["n_mirror"] for v in run.views)
+        skipped += sum(M - s["gather_sent"] for s in g["fwd"] + g["bwd"][:-1])
+    assert skipped > 0
+    run.close()
