@@ -234,9 +234,11 @@ typedef struct {
  * (boundary rows from the cached aggregate; interior rows untouched).
  * eps: cache threshold (ignored with cache_on = 0).  st (host, may be NULL):
  * counters of this call — non-NULL forces a stream synchronisation.
- * With world > 1 the call synchronises `stream` twice (NCCL message counts).
- * Errors: l/dir/ld out of range -> EUSAGE; message count above the halo
- * capacity -> EPROTO; NCCL failure -> ENCCL. */
+ * Host synchronisation: none with the slot layout (co-resident parts, NVLink push: the
+ * transfer barrier is a stream-ordered NCCL all-reduce); with the NCCL send/recv transport
+ * the call synchronises `stream` twice (message counts).
+ * Errors: l/dir/ld out of range -> EUSAGE; message count above the halo capacity or an
+ * unknown position (compacted layout) -> EPROTO; NCCL failure -> ENCCL. */
 int cdfgnn_halo_exchange(cdfgnn_ctx* ctx, int32_t l, int32_t dir, float* const* X, int64_t ld,
                          float eps, cdfgnn_sync_stats* st, void* stream);
 
