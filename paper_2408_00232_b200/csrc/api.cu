@@ -157,6 +157,7 @@ struct cdfgnn_ctx {
     unsigned long long* stats_d = nullptr;    // [L][2][4]
     unsigned long long* stats_h = nullptr;    // pinned
     double* loss_d = nullptr;        // [k]
+    double* loss_part = nullptr;     // [148] partial sums of the row losses
     int32_t* scal_d = nullptr;       // [0] correct, [1] err, [2] ntrain
     double* host_scratch = nullptr;  // pinned: k doubles + ints
     int64_t ntrain = -1;
@@ -478,6 +479,7 @@ void carve(cdfgnn_ctx* c, Bump& b) {
     }
     c->stats_d = b.take<unsigned long long>(CDFGNN_MAX_LAYERS * 2 * 4);
     c->loss_d = b.take<double>(std::max(c->k, 1));
+    c->loss_part = b.take<double>(148);
     c->scal_d = b.take<int32_t>(8);
 }
 
@@ -1560,8 +1562,8 @@ static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const
         LocalPart& P = c->parts[t];
         launch_loss(P.act[L], ldL, C, P.n, P.B, P.M, labels[t], train[t], 1.0 / (double)c->ntrain,
                     P.D[L & 1], P.rowloss, c->scal_d, c->scal_d + 1, s);
-        launch_reduce_rows(P.rowloss, P.n, c->loss_d + t, s);
-        c->launches += 2;
+        launch_reduce_rows(P.rowloss, P.n, c->loss_d + t, c->loss_part, s);
+        c->launches += 3;
         dcur[t] = P.D[L & 1];
     }
     CDF_TRY(check_launch("loss"));

@@ -196,7 +196,8 @@ void launch_relu(const float* Z, float* H, int64_t count, cudaStream_t s);
 void launch_loss(const float* logits, int64_t ld, int C, int64_t n, int64_t B, int64_t M,
                  const int32_t* labels, const uint8_t* train, double inv_ntrain, float* dlogits,
                  float* rowloss, int* correct, int* err, cudaStream_t s);
-void launch_reduce_rows(const float* rowloss, int64_t n, double* out, cudaStream_t s);
+// out = Σ rowloss[0..n) in fp64, fixed order (part: scratch of 148 doubles); two launches
+void launch_reduce_rows(const float* rowloss, int64_t n, double* out, double* part, cudaStream_t s);
 void launch_count_train(int64_t n, int64_t B, int64_t M, const uint8_t* train, int* out,
                         cudaStream_t s);
 // err (device, may be NULL): the update is skipped when *err != 0 (protocol / data error)

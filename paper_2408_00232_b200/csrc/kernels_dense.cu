@@ -208,17 +208,22 @@ __global__ void __launch_bounds__(256) loss_kernel(const float* __restrict__ log
     if (threadIdx.x == 0 && s_cnt) atomicAdd(correct, s_cnt);
 }
 
-__global__ void reduce_rows_kernel(const float* __restrict__ x, int64_t n, double* out) {
+// Σ rowloss in fp64 in a fixed order: block b sums the contiguous chunk b (8 loads in flight per
+// thread, tree over the block), then one block adds the kRedBlocks partial sums in block order
+constexpr int kRedBlocks = 148;
+__global__ void __launch_bounds__(1024) reduce_rows_kernel(const float* __restrict__ x, int64_t n,
+                                                           double* __restrict__ part) {
     __shared__ double sh[1024];
-    // 8 independent loads in flight per thread; partial sums combined in a fixed order
+    const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
     constexpr int U = 8;
     double acc[U] = {0, 0, 0, 0, 0, 0, 0, 0};
     const int64_t step = (int64_t)blockDim.x * U;
-    for (int64_t i0 = threadIdx.x; i0 < n; i0 += step) {
+    for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += step) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t i = i0 + (int64_t)u * blockDim.x;
-            if (i < n) acc[u] += (double)__ldg(x + i);
+            if (i < hi) acc[u] += (double)__ldg(x + i);
         }
     }
     double s = 0.0;
@@ -230,7 +235,15 @@ __global__ void reduce_rows_kernel(const float* __restrict__ x, int64_t n, doubl
         if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
         __syncthreads();
     }
-    if (threadIdx.x == 0) *out = sh[0];
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void reduce_parts_kernel(const double* __restrict__ part, int np, double* out) {
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int b = 0; b < np; ++b) s += part[b];
+        *out = s;
+    }
 }
 
 __global__ void count_train_kernel(int64_t n, int64_t B, int64_t M, const uint8_t* train, int* out) {
@@ -354,8 +367,9 @@ void launch_loss(const float* logits, int64_t ld, int C, int64_t n, int64_t B, i
                                                         inv_ntrain, dlogits, rowloss, correct, err);
 }
 
-void launch_reduce_rows(const float* rowloss, int64_t n, double* out, cudaStream_t s) {
-    reduce_rows_kernel<<<1, 1024, 0, s>>>(rowloss, n, out);
+void launch_reduce_rows(const float* rowloss, int64_t n, double* out, double* part, cudaStream_t s) {
+    reduce_rows_kernel<<<kRedBlocks, 1024, 0, s>>>(rowloss, n, part);
+    reduce_parts_kernel<<<1, 32, 0, s>>>(part, kRedBlocks, out);
 }
 
 void launch_count_train(int64_t n, int64_t B, int64_t M, const uint8_t* train, int* out,
