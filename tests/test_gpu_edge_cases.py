@@ -94,3 +94,22 @@ def test_epoch_with_parts_without_boundary():
         o_ = orc.epoch()
         assert abs(g["loss"] - o_["loss"]) <= 1e-5 * max(1.0, abs(o_["loss"]))
     run.close()
+
+
+def test_maximum_classes_epoch():
+    """256 classes (the loss kernel's maximum, 8 per lane): 3 exact-mode epochs, 2 parts,
+    against the oracle (loss 1e-5, W row-normwise 1e-4)."""
+    require_gpu()
+    from tests.gpu_util import rownorm_err
+    d = small_random_graph(1500, 7000, (12, 32, 256), seed=85)
+    kw = dict(cache=True, quant_bits=0, eps0=0.0, adaptive=False, optimizer="sgd", lr=0.5)
+    run = Run(d, 2, **kw)
+    orc = PartitionedGCN(opartition(d.n, d.eu, d.ev, PartitionCfg(p=2)), d.X, d.y, d.train, d.W, TrainCfg(**kw))
+    for ep in range(3):
+        g = run.epoch()
+        o = orc.epoch()
+        assert abs(g["loss"] - o["loss"]) <= 1e-5 * max(1.0, abs(o["loss"]))
+        assert g["correct"] == o["correct"]
+        for wg, wo in zip(run.weights(), orc.W):
+            assert rownorm_err(wg, wo) <= 1e-4
+    run.close()

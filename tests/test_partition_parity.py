@@ -100,3 +100,25 @@ def test_input_errors():
     with pytest.raises(cg.CdfgnnError) as e:
         cg.partition(3, np.array([0], np.int32), np.array([1], np.int32), 0)
     assert e.value.code == 2            # p < 1 -> EUSAGE
+
+
+def test_context_usage_errors_without_gpu():
+    """Config validation happens on the host (cdfgnn_workspace_size, no device touched): layer
+    widths above 1024, more than 256 classes, message widths other than 0/4/8/16 bits, an empty
+    edge list, and k outside [1, p] are EUSAGE."""
+    from synth import small_random_graph
+    d = small_random_graph(200, 800, (8, 16, 4), seed=3)
+    plan = cg.partition(d.n, d.eu, d.ev, 2)
+    ok = cg.cfg_default((8, 16, 256))
+    assert cg.workspace_size(plan, [0, 1], ok) > 0                 # 256 classes: the maximum
+    for dims, kw in (((8, 1025, 4), {}), ((8, 16, 257), {}), ((8, 16, 4), {"quant_bits": 12}),
+                     ((8, 16, 4), {"quant_bits": 2}), ((8, 16, 4), {"msg_layout": 3})):
+        with pytest.raises(cg.CdfgnnError) as e:
+            cg.workspace_size(plan, [0, 1], cg.cfg_default(dims, **kw))
+        assert e.value.code == 2, (dims, kw)
+    with pytest.raises(cg.CdfgnnError) as e:
+        cg.workspace_size(plan, [0, 1, 2], cg.cfg_default((8, 16, 4)))
+    assert e.value.code == 2                                         # k > p
+    with pytest.raises(cg.CdfgnnError) as e:
+        cg.partition(3, np.zeros(0, np.int32), np.zeros(0, np.int32), 2)
+    assert e.value.code == 2                                         # m == 0 (S:L143)
