@@ -196,6 +196,7 @@ struct cdfgnn_ctx {
     cudaStream_t s3 = nullptr;
     cudaEvent_t evG = nullptr, evJ = nullptr;
     bool dw_pending = false;
+    bool relu_z = false;               // the sync in flight writes σ(Z) (fused ReLU, fwd_impl)
 };
 
 namespace {
@@ -779,6 +780,7 @@ void sync_args(cdfgnn_ctx* c, int l, int dir, float* const* X, int64_t ld, float
         a.stride = slot_stride(bits, ld);
         a.gstamp = c->stamp[l - 1][dir][0];
         a.sstamp = c->stamp[l - 1][dir][1];
+        a.relu = (c->relu_z && dir == 0) ? 1 : 0;
     }
 }
 
@@ -984,14 +986,14 @@ int read_stats_now(cdfgnn_ctx* c, int l, int dir, int64_t wire, cudaStream_t s,
 
 // rows: 0 = all rows (longest first), 1 = mirror rows only, 2 = master + interior rows only
 int spmm_part(cdfgnn_ctx* c, LocalPart& P, const float* T, float* Y, int64_t ld, cudaStream_t s,
-              int rows = 0, const GatherFuse* gf = nullptr) {
+              int rows = 0, const GatherFuse* gf = nullptr, int64_t relu_row0 = INT64_MAX) {
     const SpmmPlan& S = spmm_plan(P, ld);
     const int64_t n = rows == 0 ? S.n_items : (rows == 1 ? S.n_items_mir : S.n_items - S.n_items_mir);
     if (n <= 0) return CDFGNN_OK;
     mark(c, PH_SPMM, s, ld);
     // column slices (CDFGNN_SPMM_CSLICE = slice width): each pass gathers an L2-sized slice of T
     const int cslice = env_knob("CDFGNN_SPMM_CSLICE", 0);
-    if (cslice > 0 && ld > cslice && rows == 0 && cslice % 4 == 0 && !gf) {
+    if (cslice > 0 && ld > cslice && rows == 0 && cslice % 4 == 0 && !gf && relu_row0 == INT64_MAX) {
         for (int64_t c0 = 0; c0 < ld; c0 += cslice) {
             const int64_t w = std::min<int64_t>(ld - c0, cslice);
             const SpmmPlan& Sw = spmm_plan(P, w);
@@ -1001,7 +1003,7 @@ int spmm_part(cdfgnn_ctx* c, LocalPart& P, const float* T, float* Y, int64_t ld,
         }
         return check_launch("spmm");
     }
-    launch_spmm(P.rowptr, P.colidx, P.val, n, spmm_items(P, rows, ld), T, Y, ld, s, 0, gf);
+    launch_spmm(P.rowptr, P.colidx, P.val, n, spmm_items(P, rows, ld), T, Y, ld, s, 0, gf, relu_row0);
     c->launches++;
     return check_launch("spmm");
 }
@@ -1066,6 +1068,13 @@ int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, cons
         c->launches += launch_transpose(W, Fi, Fo, Fo, Wt, ldwt, s);
     }
     const bool fuse = !ov && !hz && fuse_gather_on(c) && env_knob("CDFGNN_SPMM_CSLICE", 0) == 0;
+    // σ fused (R3): in place (H_out == Z), interior rows by the SpMM epilogue, boundary rows by the
+    // slot-layout master / mirror kernels; the K-major Hᵀ path and the hoisted layer keep the
+    // separate ReLU
+    bool frelu = H_out && !hz && (c->slot || c->p == 1) && env_knob("CDFGNN_SPMM_CSLICE", 0) == 0 &&
+                 env_knob("CDFGNN_FUSE_RELU", 1) != 0;
+    for (int t = 0; frelu && t < c->k; ++t)
+        frelu = H_out[t] == Z[t] && !(c->parts[t].hT[l] && c->in_epoch && !wgrad_mn());
     std::vector<SyncArgs> fargs;
     if (fuse) {
         if (ld_out != ld_of(Fo)) CDF_FAIL(CDFGNN_EUSAGE, "ld %lld must equal roundup(F, 4)", (long long)ld_out);
@@ -1089,16 +1098,18 @@ int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, cons
         }
         c->launches++;
         CDF_TRY(check_launch("gemm fwd"));
+        const int64_t r0 = frelu ? P.B + P.M : INT64_MAX;
         if (fuse) {
             GatherFuse gf;
             gf.h = halo_for(c, P, l, 0);
             gf.a = fargs[t];
             gf.dst = P.gdst;
-            CDF_TRY(spmm_part(c, P, P.T, Z[t], ld_out, s, 0, &gf));
+            CDF_TRY(spmm_part(c, P, P.T, Z[t], ld_out, s, 0, &gf, r0));
         } else if (!hz) {
-            CDF_TRY(spmm_part(c, P, P.T, Z[t], ld_out, s, ov ? 1 : 0));
+            CDF_TRY(spmm_part(c, P, P.T, Z[t], ld_out, s, ov ? 1 : 0, nullptr, r0));
         }
     }
+    c->relu_z = frelu;
     if (fuse) {
         // the gather ran in the SpMM epilogues: count its senders, transfer barrier, then the
         // master apply and scatter (Alg. 2 L10-L22)
@@ -1115,12 +1126,15 @@ int fwd_impl(cdfgnn_ctx* c, int l, const float* const* H_in, int64_t ld_in, cons
     } else if (ov) {
         // §8 f1: the mirror rows are done — their gather runs on s2 under the remaining SpMM rows
         CDF_TRY(launch_gather_async(c, l, 0, Z, ld_out, eps, s, wire));
-        for (int t = 0; t < c->k; ++t) CDF_TRY(spmm_part(c, c->parts[t], c->parts[t].T, Z[t], ld_out, s, 2));
+        for (int t = 0; t < c->k; ++t)
+            CDF_TRY(spmm_part(c, c->parts[t], c->parts[t].T, Z[t], ld_out, s, 2, nullptr,
+                              frelu ? c->parts[t].B + c->parts[t].M : INT64_MAX));
         CDF_TRY(halo_join_finish(c, l, 0, Z, ld_out, eps, s, wire, elide && l == c->cfg.L));
     } else {
         CDF_TRY(halo_impl(c, l, 0, Z, ld_out, eps, s, wire, false, elide && l == c->cfg.L));
     }
-    if (H_out) {
+    c->relu_z = false;
+    if (H_out && !frelu) {
         mark(c, PH_OTHER, s);
         for (int t = 0; t < c->k; ++t) {
             LocalPart& P = c->parts[t];
@@ -1467,6 +1481,7 @@ extern "C" int cdfgnn_halo_exchange(cdfgnn_ctx* c, int32_t l, int32_t dir, float
     if (!c || !X) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
     if (l < 1 || l > c->cfg.L || dir < 0 || dir > 1) CDF_FAIL(CDFGNN_EUSAGE, "bad layer/dir");
     cudaStream_t s = (cudaStream_t)stream;
+    c->relu_z = false;
     CUDA_TRY(cudaSetDevice(c->device));
     unsigned long long* slot = c->stats_d + ((l - 1) * 2 + dir) * 4;
     if (st) CUDA_TRY(cudaMemsetAsync(slot, 0, sizeof(long long) * 4, s));
@@ -1482,6 +1497,7 @@ extern "C" int cdfgnn_layer_fwd(cdfgnn_ctx* c, int32_t l, const float* const* H_
     if (!c || !H_in || !W || !Z) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
     if (l < 1 || l > c->cfg.L) CDF_FAIL(CDFGNN_EUSAGE, "bad layer");
     cudaStream_t s = (cudaStream_t)stream;
+    c->relu_z = false;
     CUDA_TRY(cudaSetDevice(c->device));
     unsigned long long* slot = c->stats_d + ((l - 1) * 2) * 4;
     if (st) CUDA_TRY(cudaMemsetAsync(slot, 0, sizeof(long long) * 4, s));
@@ -1498,6 +1514,7 @@ extern "C" int cdfgnn_layer_bwd(cdfgnn_ctx* c, int32_t l, float* const* dZ, int6
     if (!c || !dZ || !H_in || !W || !dW) CDF_FAIL(CDFGNN_EUSAGE, "NULL argument");
     if (l < 1 || l > c->cfg.L) CDF_FAIL(CDFGNN_EUSAGE, "bad layer");
     cudaStream_t s = (cudaStream_t)stream;
+    c->relu_z = false;
     CUDA_TRY(cudaSetDevice(c->device));
     unsigned long long* slot = c->stats_d + ((l - 1) * 2 + 1) * 4;
     if (st) CUDA_TRY(cudaMemsetAsync(slot, 0, sizeof(long long) * 4, s));
@@ -1512,6 +1529,7 @@ static int epoch_impl(cdfgnn_ctx* c, const float* const* X, const int32_t* const
                       cudaStream_t s) {
     const int L = c->cfg.L, k = c->k;
     const int C = c->cfg.dims[L];
+    c->relu_z = false;
     c->launches = 0;
     c->ev_used = 0;
     std::memset(c->pend, 0, sizeof(c->pend));

@@ -108,6 +108,7 @@ struct SyncArgs {
     int64_t rowb;         // code_row_bytes(quant, ld)
     int64_t stride;       // slot layout: slot_stride(quant, ld)
     uint32_t gstamp, sstamp;   // slot layout: stamps of this sync's gather / scatter messages
+    int relu;             // slot layout: the synced Z rows are written as σ(Z) = max(Z, 0) (R3, fused)
     CacheDev c;
     unsigned long long* stats;  // [4]: gather_sent, master_fired, active, scatter_msgs
 };
@@ -157,9 +158,11 @@ struct GatherFuse {
 };
 // width (<= 1024, % 4 == 0; default ld): the columns computed; ld: row stride of T and Y.  Split-row
 // partials are width floats per slot.  gf (optional): fuse the gather into the epilogue.
+// relu_row0: rows >= relu_row0 (the interior rows) are written as max(Z, 0) — σ fused (R3); the
+// boundary rows keep their raw partials for the synchronisation
 void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val, int64_t n_items,
                  const SpmmItems& it, const float* T, float* Y, int64_t ld, cudaStream_t s, int64_t width = 0,
-                 const GatherFuse* gf = nullptr);
+                 const GatherFuse* gf = nullptr, int64_t relu_row0 = INT64_MAX);
 // stats[0] += number of set flags (uint8) among n (the fused gather's sent count)
 void launch_count_flags(const uint8_t* f, int64_t n, unsigned long long* out, cudaStream_t s);
 

@@ -1011,7 +1011,7 @@ __device__ __forceinline__ void master_slot_row(const HaloDev& h, const SyncArgs
 #pragma unroll
         for (int v = 0; v < VPL; ++v) {
             const int c0 = (gl + v * LPR) * 4;
-            if (c0 < a.ld) st4(xr + c0, b[v]);      // Z row from the cached value
+            if (c0 < a.ld) st4(xr + c0, a.relu ? relu4(b[v]) : b[v]);   // Z row from the cached value
         }
         if (gl == 0) {
             h.fired[r] = fired ? 1 : 0;
@@ -1113,7 +1113,7 @@ __global__ void __launch_bounds__(kThreads) mirror_slot_kernel(HaloDev h, SyncAr
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
         const int c0 = (gl + v * LPR) * 4;
-        if (c0 < a.ld) st4(xr + c0, b[v]);
+        if (c0 < a.ld) st4(xr + c0, a.relu ? relu4(b[v]) : b[v]);
     }
 }
 

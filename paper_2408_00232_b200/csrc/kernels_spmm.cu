@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n_items, const i
                                                         const float* __restrict__ T,
                                                         float* __restrict__ Y, int64_t ld, int64_t width,
                                                         SpmmItems it, int stream,
-                                                        const __grid_constant__ GatherFuse gf) {
+                                                        const __grid_constant__ GatherFuse gf, int64_t relu_row0) {
     constexpr int GPW = 32 / LPR;
     const int lane = threadIdx.x & 31;
     const int g = lane / LPR, gl = lane % LPR;
@@ -184,11 +184,15 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(int64_t n_items, const i
         if (gl == 0) it.counter[pbase] = 0;     // re-armed for the next launch
     }
     float* yr = Y + row * ld;
+    const bool relu = row >= relu_row0;
 #pragma unroll
     for (int v = 0; v < VPL; ++v)
         if (colok[v]) {
             float4* yp = reinterpret_cast<float4*>(yr + (gl + v * LPR) * 4);
-            if (stream) __stcs(yp, acc[v]); else *yp = acc[v];
+            const float4 o = relu ? make_float4(fmaxf(acc[v].x, 0.f), fmaxf(acc[v].y, 0.f), fmaxf(acc[v].z, 0.f),
+                                                fmaxf(acc[v].w, 0.f))
+                                  : acc[v];
+            if (stream) __stcs(yp, o); else *yp = o;
         }
     if constexpr (FUSE) {
         // a mirror row: the following synchronisation's gather (Alg. 2 L3-L9) from registers
@@ -218,21 +222,21 @@ __global__ void count_flags_kernel(const uint8_t* __restrict__ f, int64_t n, uns
 template <int LPR, int VPL, int UNR>
 void launch(int64_t n, const int32_t* rowptr, const int32_t* colidx, const float* val, const float* T, float* Y,
             int64_t ld, int64_t width, const SpmmItems& it, cudaStream_t s, int tail, int stream,
-            const GatherFuse* gf) {
+            const GatherFuse* gf, int64_t relu_row0) {
     const int64_t rows_per_block = (kThreads / 32) * (32 / LPR);
     const unsigned grid = (unsigned)((n + rows_per_block - 1) / rows_per_block);
     static const GatherFuse none{};
     const GatherFuse& g = gf ? *gf : none;
     if (gf) {
         if (tail)
-            spmm_kernel<LPR, VPL, UNR, 1, true><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream, g);
+            spmm_kernel<LPR, VPL, UNR, 1, true><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream, g, relu_row0);
         else
-            spmm_kernel<LPR, VPL, UNR, 0, true><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream, g);
+            spmm_kernel<LPR, VPL, UNR, 0, true><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream, g, relu_row0);
     } else {
         if (tail)
-            spmm_kernel<LPR, VPL, UNR, 1, false><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream, g);
+            spmm_kernel<LPR, VPL, UNR, 1, false><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream, g, relu_row0);
         else
-            spmm_kernel<LPR, VPL, UNR, 0, false><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream, g);
+            spmm_kernel<LPR, VPL, UNR, 0, false><<<grid, kThreads, 0, s>>>(n, rowptr, colidx, val, T, Y, ld, width, it, stream, g, relu_row0);
     }
 }
 
@@ -264,7 +268,7 @@ void launch_count_flags(const uint8_t* f, int64_t n, unsigned long long* out, cu
 
 void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val, int64_t n_items,
                  const SpmmItems& it, const float* T, float* Y, int64_t ld, cudaStream_t s, int64_t width,
-                 const GatherFuse* gf) {
+                 const GatherFuse* gf, int64_t relu_row0) {
     if (n_items <= 0) return;
     if (width <= 0) width = ld;
     const int nv = (int)(width / 4);   // float4 per row (width % 4 == 0, width <= 1024)
@@ -272,35 +276,35 @@ void launch_spmm(const int32_t* rowptr, const int32_t* colidx, const float* val,
     const int tail = env_int("CDFGNN_SPMM_TAIL", width > 64 ? 1 : 0);   // predicated tail for wide rows
     // narrow rows: stream the CSR arrays and the output past L2 (evict-first), keeping T's lines
     const int stream = env_int("CDFGNN_SPMM_STREAM", width <= 64 ? 1 : 0);
-    if (nv <= 2) launch<2, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
-    else if (nv <= 4) launch<4, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
-    else if (nv <= 8) launch<8, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+    if (nv <= 2) launch<2, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
+    else if (nv <= 4) launch<4, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
+    else if (nv <= 8) launch<8, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
     else if (nv <= 16) {
         // 8 lanes x 2 float4 per row, 8 neighbours in flight, predicated tail batch: at ld = 44
         // (C3's 41 classes) 1.75 -> 1.48 ms per launch vs 16 lanes x 1 (p = 1, tools/spmm_bench.py,
         // profiles/r1); 4x3 and 2x6 were slower (fewer neighbours in flight per lane)
         const int shape = env_int("CDFGNN_SPMM_SHAPE", 3);
-        if (shape == 1 && nv <= 12) launch<4, 3, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf);
-        else if (shape == 2 && nv <= 12) launch<2, 6, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf);
-        else if (shape == 3) launch<8, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf);
-        else if (shape == 4) launch<16, 1, 16>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf);
-        else if (shape == 5) launch<4, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf);
-        else if (shape == 6) launch<8, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf);
-        else if (unr == 4) launch<16, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
-        else launch<16, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+        if (shape == 1 && nv <= 12) launch<4, 3, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf, relu_row0);
+        else if (shape == 2 && nv <= 12) launch<2, 6, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf, relu_row0);
+        else if (shape == 3) launch<8, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf, relu_row0);
+        else if (shape == 4) launch<16, 1, 16>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf, relu_row0);
+        else if (shape == 5) launch<4, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf, relu_row0);
+        else if (shape == 6) launch<8, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, 1, stream, gf, relu_row0);
+        else if (unr == 4) launch<16, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
+        else launch<16, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
     } else if (nv <= 32) {
-        if (unr == 4) launch<32, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
-        else launch<32, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+        if (unr == 4) launch<32, 1, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
+        else launch<32, 1, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
     } else if (nv <= 64) {
         const int wshape = env_int("CDFGNN_SPMM_WSHAPE", 0);
-        if (wshape == 1) launch<16, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
-        else if (wshape == 2) launch<16, 4, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
-        else if (wshape == 3) launch<32, 2, 6>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
-        else if (unr == 2) launch<32, 2, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
-        else if (unr == 8) launch<32, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
-        else launch<32, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
-    } else if (nv <= 128) launch<32, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
-    else launch<32, 8, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf);
+        if (wshape == 1) launch<16, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
+        else if (wshape == 2) launch<16, 4, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
+        else if (wshape == 3) launch<32, 2, 6>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
+        else if (unr == 2) launch<32, 2, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
+        else if (unr == 8) launch<32, 2, 8>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
+        else launch<32, 2, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
+    } else if (nv <= 128) launch<32, 4, 4>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
+    else launch<32, 8, 2>(n_items, rowptr, colidx, val, T, Y, ld, width, it, s, tail, stream, gf, relu_row0);
 }
 
 }  // namespace cdfgnn

@@ -342,3 +342,24 @@ def test_fixed_eps_sweep_follow_mode(name, scale, eps):
         skipped += sum(M - s["gather_sent"] for s in g["fwd"] + g["bwd"][:-1])
     assert skipped > 0
     run.close()
+
+
+@pytest.mark.parametrize("p,quant", [(1, 8), (3, 8), (3, 0)])
+def test_fused_relu_is_bitwise_neutral(p, quant, monkeypatch):
+    """σ applied in the SpMM epilogue (interior rows) and the slot master / mirror kernels
+    (boundary rows) instead of a separate ReLU pass (R3): bit-identical losses and weights."""
+    require_gpu()
+    d = small_random_graph(1000, 7000, (16, 24, 20, 5), seed=86)
+    kw = dict(cache=True, quant_bits=quant, eps0=0.01, adaptive=True, optimizer="adam", lr=0.01)
+    a = Run(d, p, **kw)
+    b = Run(d, p, **kw)
+    for ep in range(4):
+        monkeypatch.setenv("CDFGNN_FUSE_RELU", "1")
+        ga = a.epoch()
+        monkeypatch.setenv("CDFGNN_FUSE_RELU", "0")
+        gb = b.epoch()
+        assert ga["loss"] == gb["loss"], (ep, ga["loss"], gb["loss"])
+        for wa, wb in zip(a.weights(), b.weights()):
+            assert np.array_equal(wa, wb)
+    a.close()
+    b.close()
