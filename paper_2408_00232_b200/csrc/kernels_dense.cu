@@ -118,26 +118,27 @@ __global__ void relu_kernel(const float* __restrict__ Z, float* __restrict__ H, 
 
 constexpr int kMaxClassPerLane = 8;   // C <= 256
 
-// one row of the loss head (warp-wide); returns 1 when the row is a correctly classified
-// train master (R16: argmax ties to the lowest class)
+// one row of the loss head by a group of LPR lanes (C <= 8·LPR: 8 logits per lane); returns 1
+// when the row is a correctly classified train master (R16: argmax ties to the lowest class)
+template <int LPR>
 __device__ __forceinline__ int loss_row(const float* __restrict__ logits, int64_t ld, int C, int64_t row,
                                         int64_t B, int64_t M, const int32_t* __restrict__ labels,
                                         const uint8_t* __restrict__ train, double inv_ntrain,
                                         float* __restrict__ dlogits, float* __restrict__ rowloss, int* err,
-                                        int lane) {
+                                        int gl, unsigned gmask) {
     const bool master = row < B || row >= B + M;
     const bool use = master && train[row];
     float* drow = dlogits + row * ld;
     if (!use) {
-        for (int c = lane; c < ld; c += 32) drow[c] = 0.f;
-        if (lane == 0) rowloss[row] = 0.f;
+        for (int c = gl; c < ld; c += LPR) drow[c] = 0.f;
+        if (gl == 0) rowloss[row] = 0.f;
         return 0;
     }
     const int y = labels[row];
     if (y < 0 || y >= C) {
-        if (lane == 0) atomicExch(err, 3);
-        for (int c = lane; c < ld; c += 32) drow[c] = 0.f;
-        if (lane == 0) rowloss[row] = 0.f;
+        if (gl == 0) atomicExch(err, 3);
+        for (int c = gl; c < ld; c += LPR) drow[c] = 0.f;
+        if (gl == 0) rowloss[row] = 0.f;
         return 0;
     }
     const float* z = logits + row * ld;
@@ -146,30 +147,30 @@ __device__ __forceinline__ int loss_row(const float* __restrict__ logits, int64_
     int amax = 0x7fffffff;
 #pragma unroll
     for (int t = 0; t < kMaxClassPerLane; ++t) {
-        const int c = lane + 32 * t;
+        const int c = gl + LPR * t;
         v[t] = c < C ? z[c] : -FLT_MAX;
         if (c < C && (v[t] > mx)) { mx = v[t]; amax = c; }
     }
-    // warp argmax, ties to the lowest class (reading R16)
+    // group argmax, ties to the lowest class (reading R16)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const float om = __shfl_xor_sync(0xffffffffu, mx, o);
-        const int oa = __shfl_xor_sync(0xffffffffu, amax, o);
+    for (int o = LPR / 2; o > 0; o >>= 1) {
+        const float om = __shfl_xor_sync(gmask, mx, o);
+        const int oa = __shfl_xor_sync(gmask, amax, o);
         if (om > mx || (om == mx && oa < amax)) { mx = om; amax = oa; }
     }
     float s = 0.f;
 #pragma unroll
     for (int t = 0; t < kMaxClassPerLane; ++t) {
-        const int c = lane + 32 * t;
+        const int c = gl + LPR * t;
         if (c < C) s += expf(v[t] - mx);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(gmask, s, o);
     const float lse = mx + logf(s);
     const float inv = (float)inv_ntrain;
 #pragma unroll
     for (int t = 0; t < kMaxClassPerLane; ++t) {
-        const int c = lane + 32 * t;
+        const int c = gl + LPR * t;
         if (c < C) {
             const float p = expf(v[t] - mx) / s;
             drow[c] = (p - (c == y ? 1.f : 0.f)) * inv;
@@ -177,29 +178,37 @@ __device__ __forceinline__ int loss_row(const float* __restrict__ logits, int64_
             drow[c] = 0.f;
         }
     }
-    for (int c = lane + 32 * kMaxClassPerLane; c < ld; c += 32) drow[c] = 0.f;
-    if (lane == (y & 31)) {
+    for (int c = gl + LPR * kMaxClassPerLane; c < ld; c += LPR) drow[c] = 0.f;
+    if (gl == (y % LPR)) {
         float vy = 0.f;
 #pragma unroll
         for (int t = 0; t < kMaxClassPerLane; ++t)
-            if (lane + 32 * t == y) vy = v[t];
+            if (gl + LPR * t == y) vy = v[t];
         rowloss[row] = lse - vy;
     }
-    return amax == y ? 1 : 0;
+    return (gl == 0 && amax == y) ? 1 : 0;
 }
 
-// warp per row over a grid-stride loop; the correct count is reduced per block and added with
-// one atomic per block (a same-address atomic per row serialised at L2: ~1.5M per C4 epoch)
+// LPR lanes per row (8 when C <= 64: four rows of a warp in flight), grid-stride loop; the correct
+// count is reduced per block and added with one atomic per block (a same-address atomic per row
+// serialised at L2: ~1.5M per C4 epoch)
+template <int LPR>
 __global__ void __launch_bounds__(256) loss_kernel(const float* __restrict__ logits, int64_t ld, int C,
                                                    int64_t n, int64_t B, int64_t M,
                                                    const int32_t* __restrict__ labels,
                                                    const uint8_t* __restrict__ train, double inv_ntrain,
                                                    float* __restrict__ dlogits,
                                                    float* __restrict__ rowloss, int* correct, int* err) {
+    constexpr int GPW = 32 / LPR;
     const int lane = threadIdx.x & 31;
+    const int g = lane / LPR, gl = lane % LPR;
+    const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (g * LPR));
     int mine = 0;
-    for (int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); row < n; row += (int64_t)gridDim.x * 8)
-        mine += loss_row(logits, ld, C, row, B, M, labels, train, inv_ntrain, dlogits, rowloss, err, lane);
+    for (int64_t row = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * GPW + g; row < n;
+         row += (int64_t)gridDim.x * 8 * GPW)
+        mine += loss_row<LPR>(logits, ld, C, row, B, M, labels, train, inv_ntrain, dlogits, rowloss, err, gl, gmask);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
     __shared__ int s_cnt;
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
@@ -363,8 +372,12 @@ void launch_loss(const float* logits, int64_t ld, int C, int64_t n, int64_t B, i
                  const int32_t* labels, const uint8_t* train, double inv_ntrain, float* dlogits,
                  float* rowloss, int* correct, int* err, cudaStream_t s) {
     if (n <= 0) return;
-    loss_kernel<<<(unsigned)std::min<int64_t>((n + 7) / 8, 148 * 8), 256, 0, s>>>(logits, ld, C, n, B, M, labels, train,
-                                                        inv_ntrain, dlogits, rowloss, correct, err);
+    if (C <= 8 * kMaxClassPerLane)
+        loss_kernel<8><<<(unsigned)std::min<int64_t>((n + 31) / 32, 148 * 8), 256, 0, s>>>(
+            logits, ld, C, n, B, M, labels, train, inv_ntrain, dlogits, rowloss, correct, err);
+    else
+        loss_kernel<32><<<(unsigned)std::min<int64_t>((n + 7) / 8, 148 * 8), 256, 0, s>>>(
+            logits, ld, C, n, B, M, labels, train, inv_ntrain, dlogits, rowloss, correct, err);
 }
 
 void launch_reduce_rows(const float* rowloss, int64_t n, double* out, double* part, cudaStream_t s) {
