@@ -447,7 +447,9 @@ def _main(args, real_stdout):
     # L2 read bandwidth on this GPU (the gather-bound SpMM's real ceiling): 64 MB resident buffer
     from paper_2408_00232_b200.api import bandwidth_probe
     probe = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
-    l2_gbs = bandwidth_probe(probe, 64 << 20, 64)
+    # best of 5 (one probe right after the timed region runs at whatever clock the power cap
+    # left: 15.7-18.0 TB/s across runs)
+    l2_gbs = max(bandwidth_probe(probe, 64 << 20, 64) for _ in range(5))
     del probe
     avg_launch_ms = sp_ms / sp_n if sp_n else None
     comp_per = sp_comp / sp_n if sp_n else None
