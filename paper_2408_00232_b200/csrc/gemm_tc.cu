@@ -10,7 +10,7 @@
 // per atom) — with the plain 128-B swizzle the accumulators came back zero.
 //
 // One CTA computes a 128 x BN fp32 tile over a K range: warp 0 issues TMA loads
-// (128-byte swizzled boxes, fp32 -> tf32 rounding in the tensor map) into a
+// (64-byte swizzled K-major boxes of 16 k, 128-byte / 32-B-atom MN-major boxes, fp32 -> tf32 rounding in the tensor map) into a
 // STAGES-deep shared-memory ring guarded by mbarriers; one elected thread of
 // warp 1 issues tcgen05.mma.cta_group::1.kind::tf32 (M = 128, N = BN, K = 8) with
 // the accumulator in TMEM and tcgen05.commit releasing ring slots; warps 2-5 read
@@ -31,7 +31,15 @@ namespace cdfgnn {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BK = 32;            // 32 tf32 = 128 bytes: one swizzle row
+#ifndef GEMM_BK
+#define GEMM_BK 16
+#endif
+// k-block: 16 tf32 = 64-byte K-major rows (64-B swizzle), so a 3xTF32 stage at N = 256 is 48 KB
+// and four stages fit where two 32-wide ones did (32 = 128-byte rows, 128-B swizzle)
+constexpr int BK = GEMM_BK;
+static_assert(BK == 16 || BK == 32, "BK is 16 or 32");
+constexpr uint32_t kKLayout = BK == 32 ? 2u : 4u;     // UMMA layout type: SWIZZLE_128B / SWIZZLE_64B
+constexpr uint32_t kKSbo = 8 * BK * 4;                 // K-major: bytes between 8-row core-matrix groups
 constexpr int kConvWarps = 4;     // 3xTF32 converter warps
 constexpr int kEpiWarps = 8;      // two epilogue warpgroups split each tile's column chunks
 constexpr int kEpiWarp0 = 2 + kConvWarps;
@@ -150,7 +158,8 @@ struct Cfg {
     static constexpr int B_BYTES = BN * BK * 4;
     static constexpr int TMA_BYTES = A_BYTES + B_BYTES;                  // fp32 (or tf32) tiles
     static constexpr int STAGE_BYTES = TMA_BYTES * (SPLIT3 ? 2 : 1);     // + lo parts for 3xTF32
-    static constexpr int STAGES = (SPLIT3 ? 196608 : 200704) / STAGE_BYTES;
+    static constexpr int STAGES_FIT = (SPLIT3 ? 196608 : 200704) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;   // 3 mbarriers per stage in 256 B
     static constexpr int EPI_BYTES = kEpiWarps * 32 * 32 * 4;            // epilogue staging (TMA store boxes)
     static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;        // double-buffered accumulator
@@ -302,10 +311,10 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         const uint32_t alo = a_base + C_::TMA_BYTES, blo = b_base + C_::TMA_BYTES;
 #pragma unroll
                         for (int kk = 0; kk < BK / 8; ++kk) {
-                            const uint64_t ah = A_MN ? smem_desc_mn(a_base + kk * 1024) : smem_desc(a_base + kk * 32, 16, 1024);
-                            const uint64_t bh = B_MN ? smem_desc_mn(b_base + kk * 1024) : smem_desc(b_base + kk * 32, 16, 1024);
-                            const uint64_t al = A_MN ? smem_desc_mn(alo + kk * 1024) : smem_desc(alo + kk * 32, 16, 1024);
-                            const uint64_t bl = B_MN ? smem_desc_mn(blo + kk * 1024) : smem_desc(blo + kk * 32, 16, 1024);
+                            const uint64_t ah = A_MN ? smem_desc_mn(a_base + kk * 1024) : smem_desc(a_base + kk * 32, 16, kKSbo, kKLayout);
+                            const uint64_t bh = B_MN ? smem_desc_mn(b_base + kk * 1024) : smem_desc(b_base + kk * 32, 16, kKSbo, kKLayout);
+                            const uint64_t al = A_MN ? smem_desc_mn(alo + kk * 1024) : smem_desc(alo + kk * 32, 16, kKSbo, kKLayout);
+                            const uint64_t bl = B_MN ? smem_desc_mn(blo + kk * 1024) : smem_desc(blo + kk * 32, 16, kKSbo, kKLayout);
                             tc_mma_tf32(dcol, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
                             tc_mma_tf32(dcol, ah, bl, idesc, 1u);
                             tc_mma_tf32(dcol, al, bh, idesc, 1u);
@@ -313,12 +322,12 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     } else {
 #pragma unroll
                         for (int kk = 0; kk < BK / 8; ++kk) {
-                            // K-major: +32 B per 8 tf32 inside the 128-B swizzle row (SBO = 8 rows)
+                            // K-major: +32 B per 8 tf32 inside the 64-/128-B swizzle row (SBO = 8 rows)
                             // MN-major: +1024 B per 8 k-rows (LBO = stride of 32-wide MN chunks)
                             const uint64_t ad = A_MN ? smem_desc_mn(a_base + kk * 1024)
-                                                     : smem_desc(a_base + kk * 32, 16, 1024);
+                                                     : smem_desc(a_base + kk * 32, 16, kKSbo, kKLayout);
                             const uint64_t bd = B_MN ? smem_desc_mn(b_base + kk * 1024)
-                                                     : smem_desc(b_base + kk * 32, 16, 1024);
+                                                     : smem_desc(b_base + kk * 32, 16, kKSbo, kKLayout);
                             tc_mma_tf32(dcol, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
                         }
                     }
@@ -589,7 +598,8 @@ bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int
     cuuint32_t es[2] = {1, 1};
     CUresult r = fn(m, raw_fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_TFLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                    mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                             : (BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B),
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
