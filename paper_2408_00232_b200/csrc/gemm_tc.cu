@@ -351,6 +351,8 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     mbar_wait(&full[s], ph);
                     float4* base = reinterpret_cast<float4*>(stA(s));
                     float4* lo = reinterpret_cast<float4*>(stA(s) + C_::TMA_BYTES);
+                    const uint32_t hi_s = smem_u32(stA(s)), lo_s = hi_s + (uint32_t)C_::TMA_BYTES;
+                    (void)hi_s; (void)lo_s; (void)base; (void)lo;
 #pragma unroll 4
                     for (int v = ct; v < NV; v += 32 * kConvWarps) {
 #if GEMM_HI_INPLACE
@@ -362,12 +364,17 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         lo[v] = l;
 #else
                         // hi = the raw fp32 word: kind::tf32 reads only its top 19 bits (truncation,
-                        // tools/tc_raw.cu), so lo = x − trunc(x) is exact and only lo is written
-                        const float4 x = base[v];
-                        float4 l;
+                        // experiments/tc_raw.cu), so lo = x − trunc(x) is exact and only lo is written.
+                        // Explicit shared-window ld/st: the generic LD/ST forms cost 1-3 % of the GEMM
+                        // phase (profiles/r2/experiments/gemm_converter_ab.txt)
+                        float4 x, l;
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(hi_s + 16u * v));
                         l.x = x.x - tf32_tr(x.x); l.y = x.y - tf32_tr(x.y);
                         l.z = x.z - tf32_tr(x.z); l.w = x.w - tf32_tr(x.w);
-                        lo[v] = l;
+                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(lo_s + 16u * v), "f"(l.x), "f"(l.y),
+                                     "f"(l.z), "f"(l.w)
+                                     : "memory");
 #endif
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to tcgen05
