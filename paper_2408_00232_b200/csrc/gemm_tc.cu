@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 
 #include "common.h"
@@ -99,6 +100,52 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the mbarrier at the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+    // default (.release.cta) semantics as CUTLASS's ClusterBarrier::arrive: .release.cluster
+    // compiles to MEMBAR.GPU + ERRBAR per arrive and halved the pair GEMM's throughput
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITC_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAITC_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// MMA completion -> the mbarrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                     smem_u32(bar)),
+                 "h"((uint16_t)3)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -152,10 +199,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int BN, bool SPLIT3>
+template <int BN, bool SPLIT3, bool PAIR = false>
 struct Cfg {
+    static constexpr int BNL = PAIR ? BN / 2 : BN;                      // B rows held by this CTA
     static constexpr int A_BYTES = BM * BK * 4;
-    static constexpr int B_BYTES = BN * BK * 4;
+    static constexpr int B_BYTES = BNL * BK * 4;
     static constexpr int TMA_BYTES = A_BYTES + B_BYTES;                  // fp32 (or tf32) tiles
     static constexpr int STAGE_BYTES = TMA_BYTES * (SPLIT3 ? 2 : 1);     // + lo parts for 3xTF32
     static constexpr int STAGES_FIT = (SPLIT3 ? 196608 : 200704) / STAGE_BYTES;
@@ -165,6 +213,14 @@ struct Cfg {
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;        // double-buffered accumulator
 };
 
+#ifndef GEMM_PAIR_DEFAULT
+#define GEMM_PAIR_DEFAULT 1
+#endif
+// CTA-pair 3xTF32 GEMMs (CDFGNN_GEMM_PAIR=0/1 overrides GEMM_PAIR_DEFAULT)
+bool gemm_pair_on() {
+    static const bool v = [] { const char* e = getenv("CDFGNN_GEMM_PAIR"); return e ? atoi(e) != 0 : GEMM_PAIR_DEFAULT != 0; }();
+    return v;
+}
 #ifndef GEMM_HI_INPLACE
 #define GEMM_HI_INPLACE 0
 #endif
@@ -193,12 +249,21 @@ struct EpiArgs {
 //                   (2 x BN columns) so the epilogue of tile i overlaps the MMAs of tile i+1
 //   warps 2-5       3xTF32 converters: fp32 tile -> tf32 hi (in place) + lo (second buffer)
 //   warps 6-9       epilogue: tcgen05.ld 32 lanes each -> mask / zero padding / split-K partial
-template <bool A_MN, bool B_MN, int BN, bool SPLIT3>
+// PAIR: a CTA pair (cluster of 2, cta_group::2) computes a 256 x BN tile — each CTA loads and
+// converts its 128 rows of A and half of B's BN rows, the leader issues M = 256 MMAs that read
+// both CTAs' shared memory, and each CTA's TMEM holds its 128 accumulator rows.  Per SM this
+// halves the B-operand reads and the converter traffic for B.
+template <bool A_MN, bool B_MN, int BN, bool SPLIT3, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmC, int M, int N, int total_kb, int kb_per_split, int m_tiles,
                  int n_tiles, int z_tiles, EpiArgs ep) {
-    using C_ = Cfg<BN, SPLIT3>;
+    using C_ = Cfg<BN, SPLIT3, PAIR>;
+    static_assert(!PAIR || SPLIT3, "the CTA pair is built for the 3xTF32 path");
+    constexpr int BMT = PAIR ? 2 * BM : BM;                 // output tile rows
+    constexpr int NCTA = PAIR ? 2 : 1;
+    const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
+    const bool leader = crank == 0;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     // stage s: [A (hi)][B (hi)][A lo][B lo]   (lo parts only with SPLIT3)
@@ -219,24 +284,32 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         for (int s = 0; s < C_::STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
-            mbar_init(&conv[s], kConvWarps);   // one arrival per converter warp
+            mbar_init(&conv[s], kConvWarps * NCTA);   // one arrival per converter warp (both CTAs)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], kEpiWarps);   // one arrival per epilogue warp
+            mbar_init(&tempty[a], kEpiWarps * NCTA);   // one arrival per epilogue warp (both CTAs)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "n"(C_::TMEM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "n"(C_::TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "n"(C_::TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();             // the peer's barriers exist before any remote arrive
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -246,7 +319,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int r = t - z * mn;
         const int nt = r / m_tiles;
         const int mt = r - nt * m_tiles;
-        m0 = mt * BM;
+        m0 = mt * BMT;
         n0 = nt * BN;
         kb0 = z * kb_per_split;
         nkb = min(total_kb, kb0 + kb_per_split) - kb0;
@@ -256,7 +329,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if (lane == 0) {
             // ---------------- TMA producer ----------------
             int it = 0;
-            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+            for (int t = blockIdx.x / NCTA; t < total_tiles; t += gridDim.x / NCTA) {
                 int m0, n0, kb0, nkb;
                 decode(t, m0, n0, kb0, nkb);
                 for (int i = 0; i < nkb; ++i, ++it) {
@@ -267,42 +340,46 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     const int k = (kb0 + i) * BK;
                     uint8_t* a = stA(s);
                     uint8_t* b = stB(s);
+                    const int ma = m0 + BM * (int)crank;             // this CTA's 128 rows of A
+                    const int nb = n0 + C_::BNL * (int)crank;        // and its BNL rows of B
                     if (!A_MN) {
-                        tma_load_2d(a, &tmA, &full[s], k, m0);                      // box {32 k, 128 m}
+                        tma_load_2d(a, &tmA, &full[s], k, ma);                      // box {BK k, 128 m}
                     } else {
 #pragma unroll
                         for (int c = 0; c < BM / 32; ++c)
-                            tma_load_2d(a + c * BK * 128, &tmA, &full[s], m0 + 32 * c, k);
+                            tma_load_2d(a + c * BK * 128, &tmA, &full[s], ma + 32 * c, k);
                     }
                     if (!B_MN) {
-                        tma_load_2d(b, &tmB, &full[s], k, n0);                      // box {32 k, BN n}
+                        tma_load_2d(b, &tmB, &full[s], k, nb);                      // box {BK k, BNL n}
                     } else {
 #pragma unroll
-                        for (int c = 0; c < BN / 32; ++c)
-                            tma_load_2d(b + c * BK * 128, &tmB, &full[s], n0 + 32 * c, k);
+                        for (int c = 0; c < C_::BNL / 32; ++c)
+                            tma_load_2d(b + c * BK * 128, &tmB, &full[s], nb + 32 * c, k);
                     }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ---------------- MMA issuer ----------------
+        if (lane == 0 && leader) {
+            // ---------------- MMA issuer (the pair's leader) ----------------
             constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
                                        ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
-                                       ((uint32_t)(BM >> 4) << 24);
+                                       ((uint32_t)(BMT >> 4) << 24);
             int it = 0, ti = 0;
-            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+            for (int t = blockIdx.x / NCTA; t < total_tiles; t += gridDim.x / NCTA, ++ti) {
                 int m0, n0, kb0, nkb;
                 decode(t, m0, n0, kb0, nkb);
                 const int acc = ti & 1;
                 const uint32_t aph = (uint32_t)(ti >> 1) & 1u;
-                mbar_wait(&tempty[acc], aph ^ 1u);         // epilogue drained this accumulator
+                if (PAIR) mbar_wait_cluster(&tempty[acc], aph ^ 1u);   // both CTAs' epilogues drained it
+                else mbar_wait(&tempty[acc], aph ^ 1u);         // epilogue drained this accumulator
                 tc_fence_after();
                 const uint32_t dcol = tmem + (uint32_t)(acc * BN);
                 for (int i = 0; i < nkb; ++i, ++it) {
                     const int s = it % C_::STAGES;
                     const uint32_t ph = (uint32_t)(it / C_::STAGES) & 1u;
-                    mbar_wait(SPLIT3 ? &conv[s] : &full[s], ph);
+                    if (PAIR) mbar_wait_cluster(&conv[s], ph);       // both CTAs' stages converted
+                    else mbar_wait(SPLIT3 ? &conv[s] : &full[s], ph);
                     tc_fence_after();
                     const uint32_t a_base = smem_u32(stA(s));
                     const uint32_t b_base = smem_u32(stB(s));
@@ -315,9 +392,15 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                             const uint64_t bh = B_MN ? smem_desc_mn(b_base + kk * 1024) : smem_desc(b_base + kk * 32, 16, kKSbo, kKLayout);
                             const uint64_t al = A_MN ? smem_desc_mn(alo + kk * 1024) : smem_desc(alo + kk * 32, 16, kKSbo, kKLayout);
                             const uint64_t bl = B_MN ? smem_desc_mn(blo + kk * 1024) : smem_desc(blo + kk * 32, 16, kKSbo, kKLayout);
-                            tc_mma_tf32(dcol, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
-                            tc_mma_tf32(dcol, ah, bl, idesc, 1u);
-                            tc_mma_tf32(dcol, al, bh, idesc, 1u);
+                            if (PAIR) {
+                                tc_mma_tf32_pair(dcol, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                                tc_mma_tf32_pair(dcol, ah, bl, idesc, 1u);
+                                tc_mma_tf32_pair(dcol, al, bh, idesc, 1u);
+                            } else {
+                                tc_mma_tf32(dcol, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                                tc_mma_tf32(dcol, ah, bl, idesc, 1u);
+                                tc_mma_tf32(dcol, al, bh, idesc, 1u);
+                            }
                         }
                     } else {
 #pragma unroll
@@ -331,9 +414,11 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                             tc_mma_tf32(dcol, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
                         }
                     }
-                    tc_commit(&empty[s]);       // slot free once these MMAs have read it
+                    if (PAIR) tc_commit_pair(&empty[s]);   // both CTAs' slots free once read
+                    else tc_commit(&empty[s]);       // slot free once these MMAs have read it
                 }
-                tc_commit(&tfull[acc]);         // accumulator complete
+                if (PAIR) tc_commit_pair(&tfull[acc]);
+                else tc_commit(&tfull[acc]);    // accumulator complete
             }
         }
     } else if (warp < kEpiWarp0) {
@@ -342,7 +427,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             const int ct = threadIdx.x - 64;                 // 0 .. 32*kConvWarps-1
             constexpr int NV = C_::TMA_BYTES / 16;           // float4 per stage (A and B)
             int it = 0;
-            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+            for (int t = blockIdx.x / NCTA; t < total_tiles; t += gridDim.x / NCTA) {
                 int m0, n0, kb0, nkb;
                 decode(t, m0, n0, kb0, nkb);
                 for (int i = 0; i < nkb; ++i, ++it) {
@@ -379,8 +464,10 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to tcgen05
                     __syncwarp();
-                    if (lane == 0)
-                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&conv[s])) : "memory");
+                    if (lane == 0) {
+                        if (PAIR) mbar_arrive_remote(&conv[s], 0);   // the leader's barrier (own CTA too)
+                        else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&conv[s])) : "memory");
+                    }
                 }
             }
         }
@@ -389,7 +476,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int q = warp & 3;             // TMEM lane quarter this warp may access
         const int eg = (warp - kEpiWarp0) >> 2;   // epilogue warpgroup: even / odd 32-column chunks
         int ti = 0;
-        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+        for (int t = blockIdx.x / NCTA; t < total_tiles; t += gridDim.x / NCTA, ++ti) {
             int m0, n0, kb0, nkb;
             decode(t, m0, n0, kb0, nkb);
             const int acc = ti & 1;
@@ -398,7 +485,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             tc_fence_after();
             // each lane holds one accumulator row (32 consecutive columns per tcgen05.ld)
             float* st = epi_smem + (warp - kEpiWarp0) * 32 * 32;     // 4 KB, 1024-B aligned
-            const int rbase = m0 + 32 * q;
+            const int rbase = m0 + BM * (int)crank + 32 * q;
             const int row = rbase + lane;
             const int64_t ldo = ep.ws ? ep.ldw : ep.ldc;
             const int z = t / (m_tiles * n_tiles);
@@ -456,17 +543,24 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0)
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc])) : "memory");
+            if (lane == 0) {
+                if (PAIR) mbar_arrive_remote(&tempty[acc], 0);
+                else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc])) : "memory");
+            }
         }
     }
     if (warp >= kEpiWarp0 && lane == 0) bulk_wait0();      // TMA stores complete before exit
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();     // the leader's MMAs have read this CTA's shared memory
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C_::TMEM_COLS)
-                     : "memory");
+        if (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C_::TMEM_COLS)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C_::TMEM_COLS)
+                         : "memory");
     }
 }
 
@@ -629,12 +723,12 @@ bool make_store_map(CUtensorMap* m, const float* base, int64_t rows, int64_t col
     return r == CUDA_SUCCESS;
 }
 
-template <bool A_MN, bool B_MN, int BN, bool SPLIT3>
+template <bool A_MN, bool B_MN, int BN, bool SPLIT3, bool PAIR = false>
 int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, int64_t M, int64_t N,
                    int64_t K, int splits, const EpiArgs& ep, cudaStream_t s) {
-    using C_ = Cfg<BN, SPLIT3>;
+    using C_ = Cfg<BN, SPLIT3, PAIR>;
     static bool attr = false;
-    auto kern = gemm_tf32_kernel<A_MN, B_MN, BN, SPLIT3>;
+    auto kern = gemm_tf32_kernel<A_MN, B_MN, BN, SPLIT3, PAIR>;
     if (!attr) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM) != cudaSuccess)
             return CDFGNN_ECUDA;
@@ -643,7 +737,8 @@ int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
     const int total_kb = (int)((K + BK - 1) / BK);
     const int kbps = (total_kb + splits - 1) / splits;
     const int zs = std::max((total_kb + kbps - 1) / kbps, 1);
-    const int mt = (int)((M + BM - 1) / BM), nt = (int)((N + BN - 1) / BN);
+    constexpr int BMT = PAIR ? 2 * BM : BM;
+    const int mt = (int)((M + BMT - 1) / BMT), nt = (int)((N + BN - 1) / BN);
     const int64_t tiles = (int64_t)mt * nt * zs;
     static int sms = 0;
     if (!sms) {
@@ -651,6 +746,35 @@ int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sms <= 0) sms = 148;
+    }
+    if (PAIR) {
+        // clusters of two CTAs (one TPC), one pair per output tile at a time; the persistent grid
+        // is the number of pairs that can be co-resident (not every TPC may host one), else the
+        // clusters of a second wave would each redo a full share of tiles
+        static int max_clusters = 0;
+        cudaLaunchConfig_t lc = {};
+        lc.blockDim = dim3(kThreads);
+        lc.dynamicSmemBytes = C_::SMEM;
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        if (!max_clusters) {
+            lc.gridDim = dim3(2 * (sms / 2));
+            int mc = 0;
+            if (cudaOccupancyMaxActiveClusters(&mc, kern, &lc) != cudaSuccess || mc <= 0) mc = sms / 2;
+            max_clusters = std::min(mc, sms / 2);
+            if (getenv("CDFGNN_GEMM_PAIR_VERBOSE")) fprintf(stderr, "gemm pair: %d co-resident clusters\n", mc);
+        }
+        const unsigned grid = (unsigned)(2 * std::min<int64_t>(tiles, max_clusters));
+        lc.gridDim = dim3(grid);
+        if (cudaLaunchKernelEx(&lc, kern, ta, tb, tc, (int)M, (int)N, total_kb, kbps, mt, nt, zs, ep) != cudaSuccess)
+            return CDFGNN_ECUDA;
+        return cudaGetLastError() == cudaSuccess ? CDFGNN_OK : CDFGNN_ECUDA;
     }
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
     kern<<<grid, kThreads, C_::SMEM, s>>>(ta, tb, tc, (int)M, (int)N, total_kb, kbps, mt, nt, zs, ep);
@@ -660,6 +784,11 @@ int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
 template <bool A_MN, bool B_MN>
 int launch_bn(int BN, bool split3, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, int64_t M,
               int64_t N, int64_t K, int splits, const EpiArgs& ep, cudaStream_t s) {
+    if (split3 && gemm_pair_on()) {
+        if (BN == 64) return launch_variant<A_MN, B_MN, 64, true, true>(ta, tb, tc, M, N, K, splits, ep, s);
+        if (BN == 128) return launch_variant<A_MN, B_MN, 128, true, true>(ta, tb, tc, M, N, K, splits, ep, s);
+        return launch_variant<A_MN, B_MN, 256, true, true>(ta, tb, tc, M, N, K, splits, ep, s);
+    }
     if (split3) {
         if (BN == 64) return launch_variant<A_MN, B_MN, 64, true>(ta, tb, tc, M, N, K, splits, ep, s);
         if (BN == 128) return launch_variant<A_MN, B_MN, 128, true>(ta, tb, tc, M, N, K, splits, ep, s);
@@ -675,6 +804,10 @@ int launch_bn(int BN, bool split3, const CUtensorMap& ta, const CUtensorMap& tb,
 #ifndef GEMM_SPLIT3_BN256
 #define GEMM_SPLIT3_BN256 1
 #endif
+// rows of B one CTA loads per stage (half of BN with the CTA pair); output tile rows
+int bn_rows(int BN, bool split3) { return split3 && gemm_pair_on() ? BN / 2 : BN; }
+int bm_tile(bool split3) { return split3 && gemm_pair_on() ? 2 * BM : BM; }
+
 int pick_bn(int64_t N, bool split3) {
     if (N <= 64) return 64;
     if (N <= 128 || (split3 && !GEMM_SPLIT3_BN256)) return 128;
@@ -721,7 +854,7 @@ int gemm_tc_fwd(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, co
                 int64_t ldc, bool split3, cudaStream_t s) {
     const int BN = pick_bn(std::max(N, ldc), split3);
     CUtensorMap ta, tb;
-    if (!make_map(&ta, A, M, K, lda, BK, BM, split3) || !make_map(&tb, Bt, N, K, ldb, BK, BN, split3))
+    if (!make_map(&ta, A, M, K, lda, BK, BM, split3) || !make_map(&tb, Bt, N, K, ldb, BK, bn_rows(BN, split3), split3))
         CDF_FAIL(CDFGNN_ECUDA, "cuTensorMapEncodeTiled failed (fwd)");
     EpiArgs ep{C, ldc, nullptr, 0, nullptr, 0, 0, 0};
     CUtensorMap tc;
@@ -734,7 +867,7 @@ int gemm_tc_bwd_data(int64_t M, int64_t N, int64_t K, const float* A, int64_t ld
                      float* C, int64_t ldc, const float* mask, int64_t ldm, bool split3, cudaStream_t s) {
     const int BN = pick_bn(std::max(N, ldc), split3);
     CUtensorMap ta, tb;
-    if (!make_map(&ta, A, M, K, lda, BK, BM, split3) || !make_map(&tb, Bk, N, K, ldb, BK, BN, split3))
+    if (!make_map(&ta, A, M, K, lda, BK, BM, split3) || !make_map(&tb, Bk, N, K, ldb, BK, bn_rows(BN, split3), split3))
         CDF_FAIL(CDFGNN_ECUDA, "cuTensorMapEncodeTiled failed (bwd data)");
     EpiArgs ep{C, ldc, mask, ldm, nullptr, 0, 0, 0};
     CUtensorMap tc;
@@ -753,9 +886,9 @@ int gemm_tc_wgrad_mn(int64_t M, int64_t N, int64_t K, const float* H, int64_t ld
     if (!make_map(&ta, H, K, M, ldh, 32, BK, split3, true) || !make_map(&tb, S, K, N, lds, 32, BK, split3, true))
         CDF_FAIL(CDFGNN_ECUDA, "cuTensorMapEncodeTiled failed (wgrad, MN-major)");
     const int64_t ldw = (N + 3) / 4 * 4;
-    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    const int64_t tiles = ((M + bm_tile(split3) - 1) / bm_tile(split3)) * ((N + BN - 1) / BN);
     const int64_t total_kb = (K + BK - 1) / BK;
-    int64_t splits = std::max<int64_t>(1, std::min<int64_t>(2 * 148 / std::max<int64_t>(tiles, 1), total_kb / 8));
+    int64_t splits = std::max<int64_t>(1, std::min<int64_t>((bm_tile(split3) == BM ? 2 * 148 : 148) / std::max<int64_t>(tiles, 1), total_kb / 8));
     while (splits > 1 && splits * M * ldw > ws_cap) splits--;
     const int kbps = (int)((total_kb + splits - 1) / splits);
     const int zs = (int)((total_kb + kbps - 1) / kbps);
@@ -775,12 +908,12 @@ int gemm_tc_wgrad(int64_t M, int64_t N, int64_t K, const float* Ht, int64_t ldh,
                   int* launches) {
     const int BN = pick_bn(N, split3);
     CUtensorMap ta, tb;
-    if (!make_map(&ta, Ht, M, K, ldh, BK, BM, split3) || !make_map(&tb, St, N, K, lds, BK, BN, split3))
+    if (!make_map(&ta, Ht, M, K, ldh, BK, BM, split3) || !make_map(&tb, St, N, K, lds, BK, bn_rows(BN, split3), split3))
         CDF_FAIL(CDFGNN_ECUDA, "cuTensorMapEncodeTiled failed (wgrad)");
     const int64_t ldw = (N + 3) / 4 * 4;
-    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    const int64_t tiles = ((M + bm_tile(split3) - 1) / bm_tile(split3)) * ((N + BN - 1) / BN);
     const int64_t total_kb = (K + BK - 1) / BK;
-    int64_t splits = std::max<int64_t>(1, std::min<int64_t>(2 * 148 / std::max<int64_t>(tiles, 1), total_kb / 8));
+    int64_t splits = std::max<int64_t>(1, std::min<int64_t>((bm_tile(split3) == BM ? 2 * 148 : 148) / std::max<int64_t>(tiles, 1), total_kb / 8));
     while (splits > 1 && splits * M * ldw > ws_cap) splits--;
     const int kbps = (int)((total_kb + splits - 1) / splits);
     const int zs = (int)((total_kb + kbps - 1) / kbps);
