@@ -10,13 +10,17 @@
 // per atom) — with the plain 128-B swizzle the accumulators came back zero.
 //
 // One CTA computes a 128 x BN fp32 tile over a K range: warp 0 issues TMA loads
-// (64-byte swizzled K-major boxes of 16 k, 128-byte / 32-B-atom MN-major boxes, fp32 -> tf32 rounding in the tensor map) into a
-// STAGES-deep shared-memory ring guarded by mbarriers; one elected thread of
-// warp 1 issues tcgen05.mma.cta_group::1.kind::tf32 (M = 128, N = BN, K = 8) with
-// the accumulator in TMEM and tcgen05.commit releasing ring slots; warps 2-5 read
-// the accumulator with tcgen05.ld (32 lanes each) and run the epilogue (mask,
-// zero padding columns, split-K partials).  Split-K partials are summed in a
-// fixed order by a separate kernel, so results are run-to-run deterministic.
+// (64-byte swizzled K-major boxes of 16 k, 128-byte / 32-B-atom MN-major boxes) into a
+// STAGES-deep shared-memory ring guarded by mbarriers; warps 2-5 split each fp32 stage into
+// tf32 hi (the raw word) + lo (3xTF32); one elected thread of warp 1 issues
+// tcgen05.mma.kind::tf32 (M = 128, N = BN, K = 8) into a double-buffered TMEM accumulator,
+// tcgen05.commit releasing ring slots; warps 6-13 read the accumulator with tcgen05.ld and run
+// the epilogue (mask, zero padding columns, split-K partials, TMA stores).  3xTF32 GEMMs run
+// on CTA pairs (PAIR: cluster of 2, cta_group::2, M = 256): each CTA loads and converts its
+// 128 rows of A and half of B, the leader issues the MMAs over both CTAs' shared memory, which
+// halves each SM's shared-memory operand and conversion traffic for B — the single-CTA
+// kernel's limit.  Split-K partials are summed in a fixed order by a separate kernel, so
+// results are run-to-run deterministic.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
