@@ -568,6 +568,25 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
 }
 
+// one warp per output element: lane j sums partials j, j+32, ... then a fixed xor tree — a fixed
+// order (run-to-run deterministic) without a 100+-long dependent load chain per element
+__global__ void splitk_sum_warp_kernel(int64_t M, int64_t N, int64_t ldw, int splits, const float* __restrict__ ws,
+                                       float* __restrict__ C, int64_t ldc, int accumulate) {
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= M * ldc) return;
+    const int64_t m = i / ldc, n = i % ldc;
+    if (n >= N) {
+        if (lane == 0) C[i] = 0.f;
+        return;
+    }
+    float v = 0.f;
+    for (int z = lane; z < splits; z += 32) v += ws[((int64_t)z * M + m) * ldw + n];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) C[i] = accumulate ? v + C[i] : v;
+}
+
 __global__ void splitk_sum_kernel(int64_t M, int64_t N, int64_t ldw, int splits, const float* __restrict__ ws,
                                   float* __restrict__ C, int64_t ldc, int accumulate) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -788,8 +807,7 @@ int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
 template <bool A_MN, bool B_MN>
 int launch_bn(int BN, bool split3, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, int64_t M,
               int64_t N, int64_t K, int splits, const EpiArgs& ep, cudaStream_t s) {
-    if (split3 && gemm_pair_on()) {
-        if (BN == 64) return launch_variant<A_MN, B_MN, 64, true, true>(ta, tb, tc, M, N, K, splits, ep, s);
+    if (split3 && gemm_pair_on() && BN >= 128) {
         if (BN == 128) return launch_variant<A_MN, B_MN, 128, true, true>(ta, tb, tc, M, N, K, splits, ep, s);
         return launch_variant<A_MN, B_MN, 256, true, true>(ta, tb, tc, M, N, K, splits, ep, s);
     }
@@ -809,8 +827,9 @@ int launch_bn(int BN, bool split3, const CUtensorMap& ta, const CUtensorMap& tb,
 #define GEMM_SPLIT3_BN256 1
 #endif
 // rows of B one CTA loads per stage (half of BN with the CTA pair); output tile rows
-int bn_rows(int BN, bool split3) { return split3 && gemm_pair_on() ? BN / 2 : BN; }
-int bm_tile(bool split3) { return split3 && gemm_pair_on() ? 2 * BM : BM; }
+// (N = 64 tiles stay single-CTA: the pair measured 10-15 % slower there)
+int bn_rows(int BN, bool split3) { return split3 && gemm_pair_on() && BN >= 128 ? BN / 2 : BN; }
+int bm_tile(int BN, bool split3) { return split3 && gemm_pair_on() && BN >= 128 ? 2 * BM : BM; }
 
 int pick_bn(int64_t N, bool split3) {
     if (N <= 64) return 64;
@@ -890,9 +909,9 @@ int gemm_tc_wgrad_mn(int64_t M, int64_t N, int64_t K, const float* H, int64_t ld
     if (!make_map(&ta, H, K, M, ldh, 32, BK, split3, true) || !make_map(&tb, S, K, N, lds, 32, BK, split3, true))
         CDF_FAIL(CDFGNN_ECUDA, "cuTensorMapEncodeTiled failed (wgrad, MN-major)");
     const int64_t ldw = (N + 3) / 4 * 4;
-    const int64_t tiles = ((M + bm_tile(split3) - 1) / bm_tile(split3)) * ((N + BN - 1) / BN);
+    const int64_t tiles = ((M + bm_tile(BN, split3) - 1) / bm_tile(BN, split3)) * ((N + BN - 1) / BN);
     const int64_t total_kb = (K + BK - 1) / BK;
-    int64_t splits = std::max<int64_t>(1, std::min<int64_t>((bm_tile(split3) == BM ? 2 * 148 : 148) / std::max<int64_t>(tiles, 1), total_kb / 8));
+    int64_t splits = std::max<int64_t>(1, std::min<int64_t>((bm_tile(BN, split3) == BM ? 2 * 148 : 148) / std::max<int64_t>(tiles, 1), total_kb / 8));
     while (splits > 1 && splits * M * ldw > ws_cap) splits--;
     const int kbps = (int)((total_kb + splits - 1) / splits);
     const int zs = (int)((total_kb + kbps - 1) / kbps);
@@ -902,7 +921,10 @@ int gemm_tc_wgrad_mn(int64_t M, int64_t N, int64_t K, const float* H, int64_t ld
     int rc = launch_bn<true, true>(BN, split3, ta, tb, tc, M, N, K, (int)splits, ep, s);
     if (rc != CDFGNN_OK) CDF_FAIL(rc, "wgrad launch failed");
     const int64_t tot = M * ldc;
-    splitk_sum_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(M, N, ldw, zs, ws, C, ldc, accumulate ? 1 : 0);
+    if (zs >= 32 && tot < 148 * 256)      // few outputs, long chains: a warp per output
+        splitk_sum_warp_kernel<<<(unsigned)((tot * 32 + 255) / 256), 256, 0, s>>>(M, N, ldw, zs, ws, C, ldc, accumulate ? 1 : 0);
+    else
+        splitk_sum_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(M, N, ldw, zs, ws, C, ldc, accumulate ? 1 : 0);
     if (launches) *launches += 2;
     return cudaGetLastError() == cudaSuccess ? CDFGNN_OK : CDFGNN_ECUDA;
 }
@@ -915,9 +937,9 @@ int gemm_tc_wgrad(int64_t M, int64_t N, int64_t K, const float* Ht, int64_t ldh,
     if (!make_map(&ta, Ht, M, K, ldh, BK, BM, split3) || !make_map(&tb, St, N, K, lds, BK, bn_rows(BN, split3), split3))
         CDF_FAIL(CDFGNN_ECUDA, "cuTensorMapEncodeTiled failed (wgrad)");
     const int64_t ldw = (N + 3) / 4 * 4;
-    const int64_t tiles = ((M + bm_tile(split3) - 1) / bm_tile(split3)) * ((N + BN - 1) / BN);
+    const int64_t tiles = ((M + bm_tile(BN, split3) - 1) / bm_tile(BN, split3)) * ((N + BN - 1) / BN);
     const int64_t total_kb = (K + BK - 1) / BK;
-    int64_t splits = std::max<int64_t>(1, std::min<int64_t>((bm_tile(split3) == BM ? 2 * 148 : 148) / std::max<int64_t>(tiles, 1), total_kb / 8));
+    int64_t splits = std::max<int64_t>(1, std::min<int64_t>((bm_tile(BN, split3) == BM ? 2 * 148 : 148) / std::max<int64_t>(tiles, 1), total_kb / 8));
     while (splits > 1 && splits * M * ldw > ws_cap) splits--;
     const int kbps = (int)((total_kb + splits - 1) / splits);
     const int zs = (int)((total_kb + kbps - 1) / kbps);
@@ -927,7 +949,10 @@ int gemm_tc_wgrad(int64_t M, int64_t N, int64_t K, const float* Ht, int64_t ldh,
     int rc = launch_bn<false, false>(BN, split3, ta, tb, tc, M, N, K, (int)splits, ep, s);
     if (rc != CDFGNN_OK) CDF_FAIL(rc, "wgrad launch failed");
     const int64_t tot = M * ldc;
-    splitk_sum_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(M, N, ldw, zs, ws, C, ldc, accumulate ? 1 : 0);
+    if (zs >= 32 && tot < 148 * 256)      // few outputs, long chains: a warp per output
+        splitk_sum_warp_kernel<<<(unsigned)((tot * 32 + 255) / 256), 256, 0, s>>>(M, N, ldw, zs, ws, C, ldc, accumulate ? 1 : 0);
+    else
+        splitk_sum_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(M, N, ldw, zs, ws, C, ldc, accumulate ? 1 : 0);
     if (launches) *launches += 2;
     return cudaGetLastError() == cudaSuccess ? CDFGNN_OK : CDFGNN_ECUDA;
 }
